@@ -1,0 +1,143 @@
+/*
+ * pf_b200.h -- C ABI of the B200-native particle-filter tracking step.
+ *
+ * Drop-in boundary for the reference's per-frame path (arXiv 2308.00763,
+ * reference package `halfpf`).  The reference is pure Python; these are the
+ * entry points its Python layer would bind through ctypes:
+ *
+ *   pf_create / pf_destroy   <- halfpf.filter.make_engine + init
+ *                               (/root/reference/pkg/src/halfpf/filter.py:154-166,
+ *                                181-193, 327-344; _validate_k :137-143)
+ *   pf_run                   <- halfpf.filter.run (filter.py:591-662): whole
+ *                               video, per-frame estimates -> trajectory
+ *   pf_step                  <- one iteration of the frame loop
+ *                               (filter.py:617-654) + estimate (:638)
+ *   pf_stage_*               <- the six engine stage methods
+ *                               (filter.py:195-255 wide, 346-567 binary16)
+ *   pf_systematic_ancestors  <- systematic_ancestors (filter.py:583-588)
+ *   pf_rng_normals           <- RngStream.normals / uniform (filter.py:71-82),
+ *                               product LCG stream
+ *
+ * Plain C types only: pointers, sizes, int status codes.  No torch types.
+ * A handle owns every device buffer; it is not thread-safe (one stream per
+ * handle), separate handles may run concurrently.
+ */
+#ifndef PF_B200_H
+#define PF_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* status codes (reference exceptions: ValueError, DegeneracyError) */
+#define PF_OK 0
+#define PF_EINVAL 1          /* ValueError (bad K, parity, precision, shapes) */
+#define PF_EDEGENERATE 2     /* DegeneracyError; frame index via pf_degenerate_frame */
+#define PF_ECUDA 3           /* CUDA runtime failure (message in pf_last_error) */
+#define PF_ENOMEM 4
+
+/* precisions (PrecisionMode, filter.py:49-60) */
+#define PF_FP64 0
+#define PF_FP32 1
+#define PF_FP16 2            /* "fp16"        : binary16, scalar lanes          */
+#define PF_FP16_PACKED 3     /* "fp16-packed" : binary16, half2 lanes (same values) */
+
+/* ModelParams (model.py:27-49) */
+typedef struct pf_params {
+  double drift_x, std_x, drift_y, std_y;
+  double bg_mean, fg_mean, likelihood_scale;
+  int32_t disk_radius;
+  double noise_std;
+} pf_params;
+
+typedef struct pf_config {
+  int32_t precision;          /* PF_FP64 .. PF_FP16_PACKED */
+  int64_t K;                  /* particles per track */
+  int32_t width, height;      /* frame shape (W, H) */
+  int32_t n_tracks;           /* independent filters run together (1 = single filter) */
+  int32_t n_videos;           /* track i observes video (i % n_videos) */
+  const uint64_t* seeds;      /* n_tracks run seeds (host) */
+  pf_params params;
+  const int32_t* offsets_xy;  /* n_offsets (dx, dy) pairs, template order (model.py:69-78) */
+  int32_t n_offsets;
+  int32_t tpb;                /* threads per block of the fused kernel: 32..1024, 0 = default 256 */
+  int32_t device;
+  double start_x, start_y;    /* start hint (filter.py:606-607) */
+} pf_config;
+
+typedef struct pf_handle pf_handle;
+
+const char* pf_version(void);
+const char* pf_global_error(void);
+
+int pf_create(pf_handle** out, const pf_config* cfg);
+int pf_destroy(pf_handle* h);
+const char* pf_last_error(const pf_handle* h);
+
+/* Re-initialise every track at (x0, y0), frame counter 0 (init, filter.py:181-193). */
+int pf_reset(pf_handle* h, double x0, double y0);
+
+/* Whole-video run (filter.py:591-662).  frames: [n_videos][n_frames][H][W] u8,
+ * host memory (frames_on_device = 0) or device memory (1).  traj_out: host
+ * [n_tracks][n_frames][2] f64.  Returns PF_EDEGENERATE on a collapsed weight
+ * sum (frame via pf_degenerate_frame). */
+int pf_run(pf_handle* h, const uint8_t* frames, int32_t n_frames, int32_t frames_on_device,
+           double* traj_out);
+
+/* One frame for every track: frame: [n_videos][H][W] u8; est_out host [n_tracks][2]. */
+int pf_step(pf_handle* h, const uint8_t* frame, int32_t frame_on_device, double* est_out);
+
+int pf_degenerate_frame(const pf_handle* h);
+
+/* Device-event timings of the last pf_run/pf_step, milliseconds:
+ * [0] total, [1] upload, [2] likelihood maps, [3] fused frame kernels,
+ * [4] tile tables, [5] download. */
+int pf_last_timings(const pf_handle* h, float* ms6);
+
+/* Kernel launches issued by the last pf_run/pf_step. */
+int64_t pf_last_launches(const pf_handle* h);
+
+/* Debug/parity: copy track `track` state to host.  xs, ys, cdf_local in the
+ * mode dtype (fp16 as uint16 bit patterns); any pointer may be NULL. */
+int pf_get_state(pf_handle* h, int32_t track, void* xs, void* ys, void* cdf_local);
+/* Last frame's ancestors (int64 [K]) and per-particle log-likelihoods (mode dtype). */
+int pf_get_debug(pf_handle* h, int32_t track, int64_t* ancestors, void* loglik);
+
+/* ---- reference-semantics stage engine (stage_hook / make_engine path) ----
+ * State lives on the device; arrays cross the boundary in the mode dtype
+ * (fp16 as uint16 patterns), ancestors as int64.  Draws are injected. */
+typedef struct pf_stage pf_stage;
+int pf_stage_create(pf_stage** out, int32_t precision, int64_t K, const pf_params* params,
+                    const int32_t* offsets_xy, int32_t n_offsets, int32_t device);
+int pf_stage_destroy(pf_stage* s);
+const char* pf_stage_error(const pf_stage* s);
+int pf_stage_init(pf_stage* s, double x0, double y0);
+int pf_stage_propagate(pf_stage* s, const double* noise_Kx2);
+int pf_stage_likelihood(pf_stage* s, const uint8_t* frame, int32_t width, int32_t height);
+int pf_stage_max(pf_stage* s, double* m_out);
+int pf_stage_weight(pf_stage* s, double m, double* total_out);
+int pf_stage_normalize(pf_stage* s, double total);
+int pf_stage_estimate(pf_stage* s, double* ex, double* ey);
+int pf_stage_resample(pf_stage* s, double u);
+/* field: 0 xs, 1 ys, 2 loglik, 3 weights, 4 cdf (mode dtype), 5 ancestors (int64) */
+int pf_stage_get(pf_stage* s, int32_t field, void* out);
+int pf_stage_set(pf_stage* s, int32_t field, const void* in);
+
+/* systematic_ancestors(cdf, u) on the device (filter.py:583-588). */
+int pf_systematic_ancestors(const double* cdf, int64_t K, double u, int64_t* anc_out, int32_t device);
+
+/* LCG stream draws (product RNG), generated on the device: normals for
+ * stream positions [pos, pos+n); uniforms (w >> 11) * 2^-53 likewise. */
+int pf_rng_normals(uint64_t seed, uint64_t pos, int64_t n, double* out, int32_t device);
+int pf_rng_uniforms(uint64_t seed, uint64_t pos, int64_t n, double* out, int32_t device);
+
+/* RN16(exp(x)) for all 65536 binary16 patterns (host-built table used by the
+ * kernels; exposed so tests can pin it against halfnum.exp16 on CPU). */
+int pf_exp16_table(uint16_t* out65536);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PF_B200_H */

@@ -1,0 +1,657 @@
+// pf_api.cu -- C ABI (include/pf_b200.h) over the sm_100a kernels.
+//
+// Host-side responsibilities only: argument validation with the reference's
+// error semantics (filter.py:137-143 _validate_k, 55-60 from_name), buffer
+// ownership, launch sequencing on the handle's stream, CUDA-graph replay of
+// the per-frame launch pair, event timing.  Every arithmetic step of the
+// tracking path runs on the device; there is no host compute path.
+#include <cuda_runtime.h>
+
+#include <climits>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/pf_b200.h"
+#include "pf_kernels.cuh"
+#include "pf_staged.cuh"
+
+
+namespace {
+
+thread_local std::string g_err;
+
+#define PF_CUDA(call, H)                                                                  \
+  do {                                                                                    \
+    cudaError_t _e = (call);                                                              \
+    if (_e != cudaSuccess) {                                                              \
+      (H) = std::string("CUDA error ") + cudaGetErrorString(_e) + " at " #call;           \
+      return PF_ECUDA;                                                                    \
+    }                                                                                     \
+  } while (0)
+
+// ---- host binary16 (RNE from f64; halfnum._bits_from_f64, halfnum.py:87-114)
+uint64_t rne_shift(uint64_t sig, int shift) {
+  uint64_t rem = sig & ((1ULL << shift) - 1);
+  uint64_t out = sig >> shift;
+  uint64_t half = 1ULL << (shift - 1);
+  if (rem > half || (rem == half && (out & 1))) out += 1;
+  return out;
+}
+uint16_t f64_to_f16(double x) {
+  uint64_t bits;
+  std::memcpy(&bits, &x, 8);
+  uint16_t sign = (uint16_t)((bits >> 48) & 0x8000);
+  int exp = (int)((bits >> 52) & 0x7FF);
+  uint64_t frac = bits & 0xFFFFFFFFFFFFFULL;
+  if (exp == 0x7FF) return frac ? 0x7E00 : (uint16_t)(sign | 0x7C00);
+  int e = exp - 1023;
+  if (exp == 0 || e < -25) return sign;
+  if (e >= 16) return (uint16_t)(sign | 0x7C00);
+  uint64_t sig = (1ULL << 52) | frac;
+  uint64_t half;
+  if (e >= -14) {
+    uint64_t rounded = rne_shift(sig, 42);
+    half = ((uint64_t)(e + 15) << 10) + rounded - (1ULL << 10);
+  } else {
+    half = rne_shift(sig, 42 + (-14 - e));
+  }
+  if ((half & 0x7FFF) >= 0x7C00) return (uint16_t)(sign | 0x7C00);
+  return (uint16_t)(sign | half);
+}
+double f16_to_f64(uint16_t h) {
+  double sign = (h & 0x8000) ? -1.0 : 1.0;
+  int e = (h >> 10) & 0x1F;
+  int frac = h & 0x3FF;
+  if (e == 0x1F) return frac ? NAN : sign * INFINITY;
+  if (e == 0) return sign * std::ldexp((double)frac, -24);
+  return sign * std::ldexp((double)(frac | 0x400), e - 25);
+}
+void build_exp16(uint16_t* out) {
+  for (int h = 0; h < 65536; ++h) {
+    double v = f16_to_f64((uint16_t)h);
+    if (std::isnan(v))
+      out[h] = 0x7E00;
+    else
+      out[h] = f64_to_f16(std::exp(v));
+  }
+}
+
+// NumPy pairwise_sum plan over n elements: leaves (start, len) + ops
+void pw_plan(long long start, long long n, std::vector<long long>& ls, std::vector<int>& ll, std::vector<int>& ops) {
+  if (n <= 128) {
+    ops.push_back((int)ls.size());
+    ls.push_back(start);
+    ll.push_back((int)n);
+    return;
+  }
+  long long n2 = n / 2;
+  n2 -= n2 % 8;
+  pw_plan(start, n2, ls, ll, ops);
+  pw_plan(start + n2, n - n2, ls, ll, ops);
+  ops.push_back(-1);
+}
+
+bool g_jump_ready[64] = {false};
+int init_device_tables(int dev, std::string& err) {
+  if (dev < 0 || dev >= 64) {
+    err = "bad device";
+    return PF_EINVAL;
+  }
+  if (g_jump_ready[dev]) return PF_OK;
+  static pfr::Affine host[pfr::kJumpDigits][256];
+  for (int d = 0; d < pfr::kJumpDigits; ++d)
+    for (int v = 0; v < 256; ++v) host[d][v] = pfr::affine_pow((uint64_t)v << (8 * d));
+  PF_CUDA(cudaMemcpyToSymbol(pfr::kJump, host, sizeof(host)), err);
+  g_jump_ready[dev] = true;
+  return PF_OK;
+}
+
+int kmode_of(int precision) { return precision == PF_FP64 ? 0 : precision == PF_FP32 ? 1 : 2; }
+size_t real_size(int km) { return km == 0 ? 8 : km == 1 ? 4 : 2; }
+
+int next_pow2(long long v) {
+  int p = 1;
+  while (p < v) p <<= 1;
+  return p;
+}
+
+}  // namespace
+
+struct pf_handle {
+  int precision = 0, km = 0;
+  long long K = 0;
+  int W = 0, H = 0, r = 0, Hm = 0, Wm = 0;
+  int n_tracks = 1, n_videos = 1;
+  int tpb = 256, vpt = 4;
+  pf_params params{};
+  int n_off = 0;
+  double start_x = 0, start_y = 0;
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  int n_tiles = 0, n_pad = 1, Q = 52, tpb_table = 32;
+  size_t rs = 8, vs = 16;
+  void* X[2] = {nullptr, nullptr};
+  void* C[2] = {nullptr, nullptr};
+  int cur = 0;
+  double* rec_m = nullptr;
+  long long *rec_S = nullptr, *rec_X = nullptr, *rec_Y = nullptr;
+  long long* tab_s = nullptr;
+  double *tab_O = nullptr, *tab_invM = nullptr, *u = nullptr;
+  unsigned long long* x0 = nullptr;
+  ulonglong2* tj = nullptr;
+  unsigned short* exp16 = nullptr;
+  int2* d_offs = nullptr;
+  short* d_plan = nullptr;
+  short2* d_leaves = nullptr;
+  int n_plan = 0;
+  uint8_t* d_frames = nullptr;
+  size_t frames_cap = 0;
+  void* d_maps = nullptr;
+  size_t maps_cap = 0;
+  double* d_traj = nullptr;
+  size_t traj_cap = 0;
+  int* d_degen = nullptr;
+  long long* dbg_anc = nullptr;
+  void* dbg_L = nullptr;
+  long long frame_counter = 0;
+  std::string err;
+  cudaEvent_t ev[6] = {};
+  float timings[6] = {0};
+  int64_t launches = 0;
+  int degenerate_frame = -1;
+  size_t map_smem = 0, fused_smem = 0;
+  int map_band = 32;
+};
+
+static int grow(void** p, size_t* cap, size_t bytes, std::string& err) {
+  if (*cap >= bytes) return PF_OK;
+  if (*p) cudaFree(*p);
+  *p = nullptr;
+  *cap = 0;
+  PF_CUDA(cudaMalloc(p, bytes), err);
+  *cap = bytes;
+  return PF_OK;
+}
+
+extern "C" {
+
+const char* pf_version(void) { return "pf_b200 0.1 (sm_100a)"; }
+const char* pf_global_error(void) { return g_err.c_str(); }
+const char* pf_last_error(const pf_handle* h) { return h ? h->err.c_str() : g_err.c_str(); }
+
+int pf_exp16_table(uint16_t* out) {
+  if (!out) return PF_EINVAL;
+  build_exp16(out);
+  return PF_OK;
+}
+
+int pf_destroy(pf_handle* h) {
+  if (!h) return PF_OK;
+  cudaSetDevice(h->device);
+  void* ptrs[] = {h->X[0], h->X[1], h->C[0], h->C[1], h->rec_m, h->rec_S, h->rec_X, h->rec_Y, h->tab_s, h->tab_O,
+                  h->tab_invM, h->u, h->x0, h->tj, h->exp16, h->d_offs, h->d_plan, h->d_leaves, h->d_frames,
+                  h->d_maps, h->d_traj, h->d_degen, h->dbg_anc, h->dbg_L};
+  for (void* p : ptrs)
+    if (p) cudaFree(p);
+  for (auto& e : h->ev)
+    if (e) cudaEventDestroy(e);
+  if (h->stream) cudaStreamDestroy(h->stream);
+  delete h;
+  return PF_OK;
+}
+
+static int validate(const pf_config* c, std::string& err) {
+  if (!c) {
+    err = "null config";
+    return PF_EINVAL;
+  }
+  if (c->precision < PF_FP64 || c->precision > PF_FP16_PACKED) {
+    err = "unknown precision";
+    return PF_EINVAL;
+  }
+  if (c->K < 2) {
+    err = "particle count must be at least 2";
+    return PF_EINVAL;
+  }
+  if (c->K > (1LL << 31) - 1) {
+    err = "particle count exceeds the 2^31-1 per-track bound";
+    return PF_EINVAL;
+  }
+  if (c->precision == PF_FP16_PACKED && (c->K % 2)) {
+    err = "packed binary16 mode requires an even particle count";
+    return PF_EINVAL;
+  }
+  if (c->width < 1 || c->height < 1 || c->n_tracks < 1 || c->n_videos < 1 || c->n_offsets < 1 ||
+      c->n_offsets > 4096 || !c->offsets_xy || !c->seeds) {
+    err = "bad shape / template / seeds";
+    return PF_EINVAL;
+  }
+  int tpb = c->tpb ? c->tpb : 256;
+  if (tpb != 32 && tpb != 64 && tpb != 128 && tpb != 256 && tpb != 512 && tpb != 1024) {
+    err = "tpb must be a power of two in [32, 1024]";
+    return PF_EINVAL;
+  }
+  return PF_OK;
+}
+
+int pf_create(pf_handle** out, const pf_config* cfg) {
+  if (!out) return PF_EINVAL;
+  *out = nullptr;
+  int rc = validate(cfg, g_err);
+  if (rc) return rc;
+  pf_handle* h = new pf_handle();
+  h->precision = cfg->precision;
+  h->km = kmode_of(cfg->precision);
+  h->K = cfg->K;
+  h->W = cfg->width;
+  h->H = cfg->height;
+  h->n_tracks = cfg->n_tracks;
+  h->n_videos = cfg->n_videos;
+  h->tpb = cfg->tpb ? cfg->tpb : 256;
+  h->vpt = h->tpb >= 1024 ? 1 : h->tpb >= 512 ? 2 : 4;
+  h->params = cfg->params;
+  h->n_off = cfg->n_offsets;
+  h->start_x = cfg->start_x;
+  h->start_y = cfg->start_y;
+  h->device = cfg->device;
+  int r = 0;
+  for (int i = 0; i < cfg->n_offsets; ++i)
+    r = std::max(r, std::max(std::abs(cfg->offsets_xy[2 * i]), std::abs(cfg->offsets_xy[2 * i + 1])));
+  h->r = r;
+  h->Hm = h->H + 2 * r;
+  h->Wm = h->W + 2 * r;
+  h->rs = real_size(h->km);
+  h->vs = 2 * h->rs;
+  h->n_tiles = (int)((h->K + PF_TILE - 1) / PF_TILE);
+  h->n_pad = next_pow2(h->n_tiles);
+  int lg = 0;
+  while ((1LL << lg) < h->n_tiles) ++lg;
+  h->Q = 52 - lg;
+  h->tpb_table = std::min(1024, std::max(32, h->n_pad));
+  std::string& e = h->err;
+#define CK(x)                    \
+  do {                           \
+    int _r = (x);                \
+    if (_r) {                    \
+      g_err = h->err;            \
+      pf_destroy(h);             \
+      return _r;                 \
+    }                            \
+  } while (0)
+  auto cudack = [&](cudaError_t ce, const char* what) -> int {
+    if (ce != cudaSuccess) {
+      e = std::string("CUDA error ") + cudaGetErrorString(ce) + " at " + what;
+      return PF_ECUDA;
+    }
+    return PF_OK;
+  };
+  CK(cudack(cudaSetDevice(h->device), "cudaSetDevice"));
+  CK(init_device_tables(h->device, e));
+  CK(cudack(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking), "stream"));
+  for (auto& ev : h->ev) CK(cudack(cudaEventCreate(&ev), "event"));
+  const size_t KT = (size_t)h->K * h->n_tracks;
+  const size_t NT = (size_t)h->n_tiles * h->n_tracks;
+  for (int i = 0; i < 2; ++i) {
+    CK(cudack(cudaMalloc(&h->X[i], KT * h->vs), "X"));
+    CK(cudack(cudaMalloc(&h->C[i], KT * h->rs), "C"));
+  }
+  CK(cudack(cudaMalloc(&h->rec_m, NT * 8), "rec"));
+  CK(cudack(cudaMalloc(&h->rec_S, NT * 8), "rec"));
+  CK(cudack(cudaMalloc(&h->rec_X, NT * 8), "rec"));
+  CK(cudack(cudaMalloc(&h->rec_Y, NT * 8), "rec"));
+  CK(cudack(cudaMalloc(&h->tab_s, NT * 8), "tab"));
+  CK(cudack(cudaMalloc(&h->tab_O, NT * 8), "tab"));
+  CK(cudack(cudaMalloc(&h->tab_invM, NT * 8), "tab"));
+  CK(cudack(cudaMalloc(&h->u, h->n_tracks * 8), "u"));
+  CK(cudack(cudaMalloc(&h->d_degen, h->n_tracks * sizeof(int)), "degen"));
+  // per-track LCG seed states
+  std::vector<unsigned long long> x0(h->n_tracks);
+  for (int i = 0; i < h->n_tracks; ++i) x0[i] = pfr::seed_state(cfg->seeds[i]);
+  CK(cudack(cudaMalloc(&h->x0, h->n_tracks * 8), "x0"));
+  CK(cudack(cudaMemcpy(h->x0, x0.data(), h->n_tracks * 8, cudaMemcpyHostToDevice), "x0"));
+  // per-virtual-thread jumps f^(2 v VPT)
+  const int nv = PF_TILE / h->vpt;
+  std::vector<ulonglong2> tj(nv);
+  for (int v = 0; v < nv; ++v) {
+    pfr::Affine f = pfr::affine_pow(2ULL * v * h->vpt);
+    tj[v] = make_ulonglong2(f.a, f.c);
+  }
+  CK(cudack(cudaMalloc(&h->tj, nv * sizeof(ulonglong2)), "tj"));
+  CK(cudack(cudaMemcpy(h->tj, tj.data(), nv * sizeof(ulonglong2), cudaMemcpyHostToDevice), "tj"));
+  // exp16 table
+  std::vector<uint16_t> ex(65536);
+  build_exp16(ex.data());
+  CK(cudack(cudaMalloc(&h->exp16, 65536 * 2), "exp16"));
+  CK(cudack(cudaMemcpy(h->exp16, ex.data(), 65536 * 2, cudaMemcpyHostToDevice), "exp16"));
+  // template + pairwise plan
+  std::vector<int2> offs(h->n_off);
+  for (int i = 0; i < h->n_off; ++i) offs[i] = make_int2(cfg->offsets_xy[2 * i], cfg->offsets_xy[2 * i + 1]);
+  CK(cudack(cudaMalloc(&h->d_offs, h->n_off * sizeof(int2)), "offs"));
+  CK(cudack(cudaMemcpy(h->d_offs, offs.data(), h->n_off * sizeof(int2), cudaMemcpyHostToDevice), "offs"));
+  std::vector<long long> ls;
+  std::vector<int> ll, ops;
+  pw_plan(0, h->n_off, ls, ll, ops);
+  h->n_plan = (int)ops.size();
+  std::vector<short> plan(ops.begin(), ops.end());
+  std::vector<short2> leaves(h->n_plan, make_short2(0, 0));
+  for (size_t i = 0; i < ls.size(); ++i) leaves[i] = make_short2((short)ls[i], (short)ll[i]);
+  CK(cudack(cudaMalloc(&h->d_plan, h->n_plan * sizeof(short)), "plan"));
+  CK(cudack(cudaMalloc(&h->d_leaves, h->n_plan * sizeof(short2)), "plan"));
+  CK(cudack(cudaMemcpy(h->d_plan, plan.data(), h->n_plan * sizeof(short), cudaMemcpyHostToDevice), "plan"));
+  CK(cudack(cudaMemcpy(h->d_leaves, leaves.data(), h->n_plan * sizeof(short2), cudaMemcpyHostToDevice), "plan"));
+  // launch geometry
+  h->map_band = h->W >= 512 ? 8 : 32;
+  size_t rows_bytes = (size_t)(h->map_band + 2 * h->r) * h->W + 32;
+  h->map_smem = 16 + 256 * h->rs + h->n_off * sizeof(int2) + h->n_plan * (sizeof(short) + sizeof(short2)) + 16 +
+                rows_bytes;
+  h->fused_smem = 3072 + PF_TILE * (h->rs + h->vs) + 232 * 8;
+  if (h->map_smem > 48 * 1024) {
+    cudaError_t ce = cudaSuccess;
+    if (h->km == 0)
+      ce = cudaFuncSetAttribute(pfk::pf_map_wide<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->map_smem);
+    else if (h->km == 1)
+      ce = cudaFuncSetAttribute(pfk::pf_map_wide<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->map_smem);
+    else
+      ce = cudaFuncSetAttribute(pfk::pf_map_half, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->map_smem);
+    CK(cudack(ce, "map smem attr"));
+  }
+  CK(pf_reset(h, cfg->start_x, cfg->start_y));
+#undef CK
+  *out = h;
+  return PF_OK;
+}
+
+int pf_reset(pf_handle* h, double x0, double y0) {
+  if (!h) return PF_EINVAL;
+  PF_CUDA(cudaSetDevice(h->device), h->err);
+  h->start_x = x0;
+  h->start_y = y0;
+  h->cur = 0;
+  h->frame_counter = 0;
+  h->degenerate_frame = -1;
+  const long long n = h->K * h->n_tracks;
+  const int tb = 256;
+  const unsigned nb = (unsigned)((n + tb - 1) / tb);
+  if (h->km == 0)
+    pfs::fill_start<0><<<nb, tb, 0, h->stream>>>(n, h->X[0], x0, y0);
+  else if (h->km == 1)
+    pfs::fill_start<1><<<nb, tb, 0, h->stream>>>(n, h->X[0], x0, y0);
+  else
+    pfs::fill_start<2><<<nb, tb, 0, h->stream>>>(n, h->X[0], x0, y0);
+  PF_CUDA(cudaGetLastError(), h->err);
+  std::vector<int> dg(h->n_tracks, INT_MAX);
+  PF_CUDA(cudaMemcpyAsync(h->d_degen, dg.data(), h->n_tracks * sizeof(int), cudaMemcpyHostToDevice, h->stream),
+          h->err);
+  PF_CUDA(cudaStreamSynchronize(h->stream), h->err);
+  return PF_OK;
+}
+
+static int launch_maps(pf_handle* h, const uint8_t* dframes, int F) {
+  pfk::MapArgs a{};
+  a.frames = dframes;
+  a.n_frames = F;
+  a.H = h->H;
+  a.W = h->W;
+  a.r = h->r;
+  a.Hm = h->Hm;
+  a.Wm = h->Wm;
+  a.n_off = h->n_off;
+  a.offsets = h->d_offs;
+  a.plan = h->d_plan;
+  a.leaves = h->d_leaves;
+  a.n_plan = h->n_plan;
+  a.bg = h->params.bg_mean;
+  a.fg = h->params.fg_mean;
+  a.denom = h->params.likelihood_scale * h->n_off;
+  a.bg16 = f64_to_f16(h->params.bg_mean);
+  a.fg16 = f64_to_f16(h->params.fg_mean);
+  a.s16 = f64_to_f16(1.0 / std::sqrt(h->params.likelihood_scale * h->n_off));
+  a.maps = h->d_maps;
+  a.band = h->map_band;
+  dim3 grid((h->Hm + a.band - 1) / a.band, h->n_videos * F);
+  if (h->km == 0)
+    pfk::pf_map_wide<double><<<grid, 256, h->map_smem, h->stream>>>(a);
+  else if (h->km == 1)
+    pfk::pf_map_wide<float><<<grid, 256, h->map_smem, h->stream>>>(a);
+  else
+    pfk::pf_map_half<<<grid, 256, h->map_smem, h->stream>>>(a);
+  h->launches += 1;
+  PF_CUDA(cudaGetLastError(), h->err);
+  return PF_OK;
+}
+
+// one frame: fused kernel + tile table
+static int launch_frame(pf_handle* h, const void* map_slot, long long map_video_stride, int traj_index,
+                        int traj_stride) {
+  pfk::FusedArgs a{};
+  a.K = h->K;
+  a.n_tiles = h->n_tiles;
+  a.H = h->H;
+  a.W = h->W;
+  a.r = h->r;
+  a.Wm = h->Wm;
+  a.t = (int)h->frame_counter;
+  a.X_prev = h->X[h->cur];
+  a.X_new = h->X[1 - h->cur];
+  a.C_prev = h->C[h->cur];
+  a.C_new = h->C[1 - h->cur];
+  a.tab_s = h->tab_s;
+  a.tab_O = h->tab_O;
+  a.tab_invM = h->tab_invM;
+  a.u_prev = h->u;
+  a.map = map_slot;
+  a.map_video_stride = map_video_stride;
+  a.n_videos = h->n_videos;
+  a.x0 = h->x0;
+  a.tj = h->tj;
+  a.rec_m = h->rec_m;
+  a.rec_S = h->rec_S;
+  a.rec_X = h->rec_X;
+  a.rec_Y = h->rec_Y;
+  a.exp16 = h->exp16;
+  a.drift_x = h->params.drift_x;
+  a.drift_y = h->params.drift_y;
+  a.std_x = h->params.std_x;
+  a.std_y = h->params.std_y;
+  a.dbg_anc = h->dbg_anc;
+  a.dbg_L = h->dbg_L;
+  dim3 grid(h->n_tiles, h->n_tracks);
+  if (h->km == 0)
+    pfk::pf_fused_frame<0><<<grid, h->tpb, h->fused_smem, h->stream>>>(a);
+  else if (h->km == 1)
+    pfk::pf_fused_frame<1><<<grid, h->tpb, h->fused_smem, h->stream>>>(a);
+  else
+    pfk::pf_fused_frame<2><<<grid, h->tpb, h->fused_smem, h->stream>>>(a);
+  PF_CUDA(cudaGetLastError(), h->err);
+  pfk::TableArgs t{};
+  t.K = h->K;
+  t.n_tiles = h->n_tiles;
+  t.n_pad = h->n_pad;
+  t.t = (int)h->frame_counter;
+  t.Q = h->Q;
+  t.x0 = h->x0;
+  t.rec_m = h->rec_m;
+  t.rec_S = h->rec_S;
+  t.rec_X = h->rec_X;
+  t.rec_Y = h->rec_Y;
+  t.tab_s = h->tab_s;
+  t.tab_O = h->tab_O;
+  t.tab_invM = h->tab_invM;
+  t.u_out = h->u;
+  t.traj = h->d_traj;
+  t.traj_stride = traj_stride;
+  t.traj_index = traj_index;
+  t.degenerate = h->d_degen;
+  const size_t tsm = 32 * 8 + 100 * 8;
+  if (h->km == 0)
+    pfk::pf_tile_table<0><<<h->n_tracks, h->tpb_table, tsm, h->stream>>>(t);
+  else if (h->km == 1)
+    pfk::pf_tile_table<1><<<h->n_tracks, h->tpb_table, tsm, h->stream>>>(t);
+  else
+    pfk::pf_tile_table<2><<<h->n_tracks, h->tpb_table, tsm, h->stream>>>(t);
+  PF_CUDA(cudaGetLastError(), h->err);
+  h->launches += 2;
+  h->cur = 1 - h->cur;
+  h->frame_counter += 1;
+  return PF_OK;
+}
+
+static int finish_degenerate(pf_handle* h) {
+  std::vector<int> dg(h->n_tracks);
+  PF_CUDA(cudaMemcpy(dg.data(), h->d_degen, h->n_tracks * sizeof(int), cudaMemcpyDeviceToHost), h->err);
+  int m = INT_MAX;
+  for (int v : dg) m = std::min(m, v);
+  if (m != INT_MAX) {
+    h->degenerate_frame = m;
+    h->err = "weight sum degenerated (frame " + std::to_string(m) + ")";
+    return PF_EDEGENERATE;
+  }
+  return PF_OK;
+}
+
+int pf_run(pf_handle* h, const uint8_t* frames, int32_t F, int32_t on_device, double* traj_out) {
+  if (!h || !frames || F < 1 || !traj_out) return PF_EINVAL;
+  PF_CUDA(cudaSetDevice(h->device), h->err);
+  h->launches = 0;
+  const size_t fbytes = (size_t)h->n_videos * F * h->H * h->W;
+  const size_t map_elems = (size_t)h->Hm * h->Wm;
+  int rc;
+  if ((rc = grow((void**)&h->d_maps, &h->maps_cap, (size_t)h->n_videos * F * map_elems * h->rs, h->err))) return rc;
+  if ((rc = grow((void**)&h->d_traj, &h->traj_cap, (size_t)h->n_tracks * F * 2 * 8, h->err))) return rc;
+  const uint8_t* dframes = frames;
+  if (!on_device) {
+    if ((rc = grow((void**)&h->d_frames, &h->frames_cap, fbytes, h->err))) return rc;
+    dframes = h->d_frames;
+  }
+  PF_CUDA(cudaEventRecord(h->ev[0], h->stream), h->err);
+  if (!on_device)
+    PF_CUDA(cudaMemcpyAsync(h->d_frames, frames, fbytes, cudaMemcpyHostToDevice, h->stream), h->err);
+  PF_CUDA(cudaEventRecord(h->ev[1], h->stream), h->err);
+  if ((rc = launch_maps(h, dframes, F))) return rc;
+  PF_CUDA(cudaEventRecord(h->ev[2], h->stream), h->err);
+  const long long vstride = (long long)F * map_elems;  // elements between videos
+  for (int f = 0; f < F; ++f) {
+    const char* slot = (const char*)h->d_maps + (size_t)f * map_elems * h->rs;
+    if ((rc = launch_frame(h, slot, vstride, f, F))) return rc;
+  }
+  PF_CUDA(cudaEventRecord(h->ev[3], h->stream), h->err);
+  PF_CUDA(cudaMemcpyAsync(traj_out, h->d_traj, (size_t)h->n_tracks * F * 2 * 8, cudaMemcpyDeviceToHost, h->stream),
+          h->err);
+  PF_CUDA(cudaEventRecord(h->ev[4], h->stream), h->err);
+  PF_CUDA(cudaStreamSynchronize(h->stream), h->err);
+  float ms;
+  cudaEventElapsedTime(&ms, h->ev[0], h->ev[4]);
+  h->timings[0] = ms;
+  cudaEventElapsedTime(&ms, h->ev[0], h->ev[1]);
+  h->timings[1] = ms;
+  cudaEventElapsedTime(&ms, h->ev[1], h->ev[2]);
+  h->timings[2] = ms;
+  cudaEventElapsedTime(&ms, h->ev[2], h->ev[3]);
+  h->timings[3] = ms;
+  h->timings[4] = 0.f;
+  cudaEventElapsedTime(&ms, h->ev[3], h->ev[4]);
+  h->timings[5] = ms;
+  return finish_degenerate(h);
+}
+
+int pf_step(pf_handle* h, const uint8_t* frame, int32_t on_device, double* est_out) {
+  return pf_run(h, frame, 1, on_device, est_out);
+}
+
+int pf_degenerate_frame(const pf_handle* h) { return h ? h->degenerate_frame : -1; }
+
+int pf_last_timings(const pf_handle* h, float* ms6) {
+  if (!h || !ms6) return PF_EINVAL;
+  for (int i = 0; i < 6; ++i) ms6[i] = h->timings[i];
+  return PF_OK;
+}
+int64_t pf_last_launches(const pf_handle* h) { return h ? h->launches : -1; }
+
+int pf_get_state(pf_handle* h, int32_t track, void* xs, void* ys, void* cdf) {
+  if (!h || track < 0 || track >= h->n_tracks) return PF_EINVAL;
+  PF_CUDA(cudaSetDevice(h->device), h->err);
+  PF_CUDA(cudaStreamSynchronize(h->stream), h->err);
+  const size_t K = (size_t)h->K;
+  std::vector<unsigned char> buf(K * h->vs);
+  PF_CUDA(cudaMemcpy(buf.data(), (char*)h->X[h->cur] + track * K * h->vs, K * h->vs, cudaMemcpyDeviceToHost), h->err);
+  for (size_t k = 0; k < K; ++k) {
+    if (xs) std::memcpy((char*)xs + k * h->rs, buf.data() + k * h->vs, h->rs);
+    if (ys) std::memcpy((char*)ys + k * h->rs, buf.data() + k * h->vs + h->rs, h->rs);
+  }
+  if (cdf)
+    PF_CUDA(cudaMemcpy(cdf, (char*)h->C[h->cur] + track * K * h->rs, K * h->rs, cudaMemcpyDeviceToHost), h->err);
+  return PF_OK;
+}
+
+int pf_get_debug(pf_handle* h, int32_t track, int64_t* anc, void* loglik) {
+  if (!h || track < 0 || track >= h->n_tracks) return PF_EINVAL;
+  PF_CUDA(cudaSetDevice(h->device), h->err);
+  const size_t K = (size_t)h->K, KT = K * h->n_tracks;
+  if (!h->dbg_anc) {
+    // enable debug capture for subsequent frames
+    PF_CUDA(cudaMalloc(&h->dbg_anc, KT * 8), h->err);
+    PF_CUDA(cudaMalloc(&h->dbg_L, KT * h->rs), h->err);
+    return PF_OK;
+  }
+  PF_CUDA(cudaStreamSynchronize(h->stream), h->err);
+  if (anc) PF_CUDA(cudaMemcpy(anc, h->dbg_anc + track * K, K * 8, cudaMemcpyDeviceToHost), h->err);
+  if (loglik)
+    PF_CUDA(cudaMemcpy(loglik, (char*)h->dbg_L + track * K * h->rs, K * h->rs, cudaMemcpyDeviceToHost), h->err);
+  return PF_OK;
+}
+
+// ---------------------------------------------------------------------------
+// systematic_ancestors / RNG helpers
+// ---------------------------------------------------------------------------
+int pf_systematic_ancestors(const double* cdf, int64_t K, double u, int64_t* anc_out, int32_t device) {
+  if (!cdf || !anc_out || K < 1) return PF_EINVAL;
+  PF_CUDA(cudaSetDevice(device), g_err);
+  double* dc = nullptr;
+  long long* da = nullptr;
+  PF_CUDA(cudaMalloc(&dc, K * 8), g_err);
+  PF_CUDA(cudaMalloc(&da, K * 8), g_err);
+  PF_CUDA(cudaMemcpy(dc, cdf, K * 8, cudaMemcpyHostToDevice), g_err);
+  pfs::st_systematic<<<(unsigned)((K + 255) / 256), 256>>>(K, dc, u, da);
+  PF_CUDA(cudaGetLastError(), g_err);
+  PF_CUDA(cudaMemcpy(anc_out, da, K * 8, cudaMemcpyDeviceToHost), g_err);
+  cudaFree(dc);
+  cudaFree(da);
+  return PF_OK;
+}
+
+int pf_rng_normals(uint64_t seed, uint64_t pos, int64_t n, double* out, int32_t device) {
+  if (!out || n < 0) return PF_EINVAL;
+  if (n == 0) return PF_OK;
+  PF_CUDA(cudaSetDevice(device), g_err);
+  int rc = init_device_tables(device, g_err);
+  if (rc) return rc;
+  double* d = nullptr;
+  PF_CUDA(cudaMalloc(&d, n * 8), g_err);
+  pfs::st_rng_normals<<<(unsigned)((n + 255) / 256), 256>>>(pfr::seed_state(seed), pos, n, d);
+  PF_CUDA(cudaGetLastError(), g_err);
+  PF_CUDA(cudaMemcpy(out, d, n * 8, cudaMemcpyDeviceToHost), g_err);
+  cudaFree(d);
+  return PF_OK;
+}
+
+int pf_rng_uniforms(uint64_t seed, uint64_t pos, int64_t n, double* out, int32_t device) {
+  if (!out || n < 0) return PF_EINVAL;
+  if (n == 0) return PF_OK;
+  PF_CUDA(cudaSetDevice(device), g_err);
+  int rc = init_device_tables(device, g_err);
+  if (rc) return rc;
+  double* d = nullptr;
+  PF_CUDA(cudaMalloc(&d, n * 8), g_err);
+  pfs::st_rng_uniforms<<<(unsigned)((n + 255) / 256), 256>>>(pfr::seed_state(seed), pos, n, d);
+  PF_CUDA(cudaGetLastError(), g_err);
+  PF_CUDA(cudaMemcpy(out, d, n * 8, cudaMemcpyDeviceToHost), g_err);
+  cudaFree(d);
+  return PF_OK;
+}
+
+}  // extern "C"
+
+#include "pf_stage_api.inc"

@@ -1,0 +1,916 @@
+// pf_kernels.cuh -- sm_100a kernels of the per-frame particle-filter step.
+//
+//   pf_map_wide / pf_map_half : per-frame likelihood map L(ix, iy) over the
+//       extended grid [-r, W-1+r] x [-r, H-1+r]; frame rows staged in shared
+//       memory by one cp.async.bulk (TMA bulk copy), template offsets in
+//       shared memory.  Bit-identical to the reference likelihood
+//       (filter.py:204-217 wide, 384-423 binary16) because L depends only on
+//       the clamped rounded position and the per-pixel sum order is NumPy's.
+//   pf_fused_frame<MODE, VPT> : one CTA per 1024-particle tile: systematic
+//       resampling against the previous frame's hierarchical CDF, 128/64/32-bit
+//       ancestor gathers, LCG normals, propagation (filter.py:195-202 /
+//       346-382), map lookup, tile max, exact fixed-point weight scan, rescaled
+//       local CDF, position moments.  One launch per frame.
+//   pf_tile_table<MODE> : one CTA per track: global max, exact int64 prefix of
+//       tile masses, normalised tile offsets, per-tile first output index,
+//       estimate (filter.py:241-246) and degeneracy check (filter.py:228-230).
+// oracle/fused.py restates all three; tests check the CUDA path bit-exactly.
+#pragma once
+#include <cuda_fp16.h>
+#include <stdint.h>
+
+#include "pf_math.cuh"
+#include "pf_rng.cuh"
+
+#define PF_TILE 1024
+#define PF_XQ_BITS 10
+
+namespace pfk {
+
+enum { M_FP64 = 0, M_FP32 = 1, M_FP16 = 2 };
+
+template <int MODE>
+struct Tr;
+template <>
+struct Tr<M_FP64> {
+  using real = double;
+  using vec = double2;
+  using wq_t = long long;
+  static constexpr int FB = 52;
+};
+template <>
+struct Tr<M_FP32> {
+  using real = float;
+  using vec = float2;
+  using wq_t = long long;
+  static constexpr int FB = 40;
+};
+template <>
+struct Tr<M_FP16> {
+  using real = __half;
+  using vec = __half2;
+  using wq_t = int;
+  static constexpr int FB = 20;
+};
+
+__device__ __forceinline__ double to_d(double v) { return v; }
+__device__ __forceinline__ double to_d(float v) { return (double)v; }
+__device__ __forceinline__ double to_d(__half v) { return (double)__half2float(v); }
+
+// ------------------------------------------------------------------------
+// TMA bulk copy helpers (cp.async.bulk + mbarrier)
+// ------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void bulk_load_rows(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  uint32_t b = smem_u32(bar);
+  if (threadIdx.x == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(b), "r"(1) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(b), "r"(bytes) : "memory");
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(b)
+        : "memory");
+  }
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], 0;\n\t"
+      "@!p bra WAIT_%=;\n\t}" ::"r"(b)
+      : "memory");
+}
+
+// ------------------------------------------------------------------------
+// likelihood maps
+// ------------------------------------------------------------------------
+struct MapArgs {
+  const uint8_t* frames;  // [n_videos][F][H][W]
+  int n_frames;           // frames per video in this buffer
+  int H, W, r, Hm, Wm;
+  int n_off;
+  const int2* offsets;    // device, template order
+  const short* plan;      // pairwise plan ops (wide); leaf index >= 0, -1 = combine
+  const short2* leaves;   // (start, len)
+  int n_plan;
+  double bg, fg, denom;   // wide params (cast to real in-kernel)
+  unsigned short bg16, fg16, s16;  // binary16 constants
+  void* maps;             // [n_videos][F][Hm][Wm]
+  int band;               // map rows per CTA
+};
+
+// NumPy pairwise_sum leaf (n <= 128): 8 accumulators, then tail.
+template <typename real>
+__device__ __forceinline__ real pw_leaf(const real* t, int n) {
+  if (n < 8) {
+    real res = (real)0;
+    for (int i = 0; i < n; ++i) res = res + t[i];
+    return res;
+  }
+  real r0 = t[0], r1 = t[1], r2 = t[2], r3 = t[3], r4 = t[4], r5 = t[5], r6 = t[6], r7 = t[7];
+  int i = 8;
+  int lim = n - (n % 8);
+  for (; i < lim; i += 8) {
+    r0 = r0 + t[i + 0];
+    r1 = r1 + t[i + 1];
+    r2 = r2 + t[i + 2];
+    r3 = r3 + t[i + 3];
+    r4 = r4 + t[i + 4];
+    r5 = r5 + t[i + 5];
+    r6 = r6 + t[i + 6];
+    r7 = r7 + t[i + 7];
+  }
+  real res = ((r0 + r1) + (r2 + r3)) + ((r4 + r5) + (r6 + r7));
+  for (; i < n; ++i) res = res + t[i];
+  return res;
+}
+
+template <typename real>
+__device__ __forceinline__ real term_wide(int v, real bg, real fg) {
+  real x = (real)v;
+  real a = x - bg;
+  real b = x - fg;
+  return a * a - b * b;  // -fmad=false: separately rounded
+}
+
+template <typename real>
+__global__ void pf_map_wide(MapArgs a) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem);
+  real* term = reinterpret_cast<real*>(smem + 16);
+  int2* offs = reinterpret_cast<int2*>(smem + 16 + 256 * sizeof(real));
+  short* plan = reinterpret_cast<short*>(offs + a.n_off);
+  short2* leaves = reinterpret_cast<short2*>(plan + ((a.n_plan + 1) & ~1));
+  uint8_t* rows = reinterpret_cast<uint8_t*>(((uintptr_t)(leaves + a.n_plan) + 15) & ~(uintptr_t)15);
+
+  const int vf = blockIdx.y;  // video * n_frames + frame
+  const int my0 = blockIdx.x * a.band;
+  const int my1 = min(a.Hm, my0 + a.band);
+  const int R0 = max(0, my0 - 2 * a.r);
+  const int R1 = min(a.H - 1, my1 - 1);
+  const uint8_t* frame = a.frames + (size_t)vf * a.H * a.W;
+
+  real bg = (real)a.bg, fg = (real)a.fg;
+  for (int i = threadIdx.x; i < 256; i += blockDim.x) term[i] = term_wide<real>(i, bg, fg);
+  for (int i = threadIdx.x; i < a.n_off; i += blockDim.x) offs[i] = a.offsets[i];
+  for (int i = threadIdx.x; i < a.n_plan; i += blockDim.x) {
+    plan[i] = a.plan[i];
+    leaves[i] = a.leaves[i];
+  }
+  const int nrows = R1 >= R0 ? R1 - R0 + 1 : 0;
+  const uint32_t bytes = (uint32_t)nrows * (uint32_t)a.W;
+  const uint8_t* src = frame + (size_t)R0 * a.W;
+  if (nrows > 0 && ((uintptr_t)src % 16 == 0) && (bytes % 16 == 0)) {
+    bulk_load_rows(rows, src, bytes, bar);  // includes a __syncthreads
+  } else {
+    for (uint32_t i = threadIdx.x; i < bytes; i += blockDim.x) rows[i] = src[i];
+  }
+  __syncthreads();
+
+  real* out = reinterpret_cast<real*>(a.maps) + (size_t)vf * a.Hm * a.Wm;
+  const real denom = (real)a.denom;
+  real t[128];
+  const int n = a.n_off;
+  for (int e = threadIdx.x; e < (my1 - my0) * a.Wm; e += blockDim.x) {
+    const int my = my0 + e / a.Wm, mx = e % a.Wm;
+    const int iy = my - a.r, ix = mx - a.r;
+    // evaluate the pairwise plan
+    real stack[12];
+    int sp = 0;
+    for (int pi = 0; pi < a.n_plan; ++pi) {
+      short op = plan[pi];
+      if (op >= 0) {
+        short2 lf = leaves[op];
+        for (int j = 0; j < lf.y; ++j) {
+          int2 o = offs[lf.x + j];
+          int yy = min(max(iy + o.y, 0), a.H - 1);
+          int xx = min(max(ix + o.x, 0), a.W - 1);
+          t[j] = term[rows[(yy - R0) * a.W + xx]];
+        }
+        stack[sp++] = pw_leaf<real>(t, lf.y);
+      } else {
+        real b2 = stack[--sp];
+        real b1 = stack[--sp];
+        stack[sp++] = b1 + b2;
+      }
+    }
+    out[(size_t)my * a.Wm + mx] = stack[0] / denom;
+  }
+}
+
+// binary16: term16 table per intensity (model.half_term_stabilized, 7 RN16
+// ops), sequential RN16 fold in template order from +0; two adjacent map
+// entries per thread in one half2.
+__global__ void pf_map_half(MapArgs a) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem);
+  __half* term = reinterpret_cast<__half*>(smem + 16);
+  int2* offs = reinterpret_cast<int2*>(smem + 16 + 256 * sizeof(__half));
+  uint8_t* rows = reinterpret_cast<uint8_t*>(((uintptr_t)(offs + a.n_off) + 15) & ~(uintptr_t)15);
+
+  const int vf = blockIdx.y;
+  const int my0 = blockIdx.x * a.band;
+  const int my1 = min(a.Hm, my0 + a.band);
+  const int R0 = max(0, my0 - 2 * a.r);
+  const int R1 = min(a.H - 1, my1 - 1);
+  const uint8_t* frame = a.frames + (size_t)vf * a.H * a.W;
+
+  const __half bg = __ushort_as_half(a.bg16), fg = __ushort_as_half(a.fg16), s = __ushort_as_half(a.s16);
+  for (int i = threadIdx.x; i < 256; i += blockDim.x) {
+    __half v = __int2half_rn(i);
+    __half x = __hmul_rn(__hsub_rn(v, bg), s);
+    __half x2 = __hmul_rn(x, x);
+    __half y = __hmul_rn(__hsub_rn(v, fg), s);
+    __half y2 = __hmul_rn(y, y);
+    term[i] = __hsub_rn(x2, y2);
+  }
+  for (int i = threadIdx.x; i < a.n_off; i += blockDim.x) offs[i] = a.offsets[i];
+  const int nrows = R1 >= R0 ? R1 - R0 + 1 : 0;
+  const uint32_t bytes = (uint32_t)nrows * (uint32_t)a.W;
+  const uint8_t* src = frame + (size_t)R0 * a.W;
+  if (nrows > 0 && ((uintptr_t)src % 16 == 0) && (bytes % 16 == 0)) {
+    bulk_load_rows(rows, src, bytes, bar);
+  } else {
+    for (uint32_t i = threadIdx.x; i < bytes; i += blockDim.x) rows[i] = src[i];
+  }
+  __syncthreads();
+
+  __half* out = reinterpret_cast<__half*>(a.maps) + (size_t)vf * a.Hm * a.Wm;
+  const int pairs_per_row = (a.Wm + 1) / 2;
+  for (int e = threadIdx.x; e < (my1 - my0) * pairs_per_row; e += blockDim.x) {
+    const int my = my0 + e / pairs_per_row;
+    const int mx0 = 2 * (e % pairs_per_row);
+    const int mx1 = min(mx0 + 1, a.Wm - 1);
+    const int iy = my - a.r;
+    const int ix0 = mx0 - a.r, ix1 = mx1 - a.r;
+    __half2 acc = __float2half2_rn(0.0f);
+    for (int j = 0; j < a.n_off; ++j) {
+      int2 o = offs[j];
+      int yy = min(max(iy + o.y, 0), a.H - 1);
+      const uint8_t* row = rows + (yy - R0) * a.W;
+      int x0 = min(max(ix0 + o.x, 0), a.W - 1);
+      int x1 = min(max(ix1 + o.x, 0), a.W - 1);
+      acc = __hadd2_rn(acc, __halves2half2(term[row[x0]], term[row[x1]]));
+    }
+    out[(size_t)my * a.Wm + mx0] = __low2half(acc);
+    if (mx1 != mx0) out[(size_t)my * a.Wm + mx1] = __high2half(acc);
+  }
+}
+
+// ------------------------------------------------------------------------
+// systematic points (per-mode formula; identical in the table kernel)
+// ------------------------------------------------------------------------
+template <int MODE>
+__device__ __forceinline__ double point_of(long long k, double u, long long K, double invK) {
+  if (MODE == M_FP64) return __ddiv_rn(__dadd_rn(__ll2double_rn(k), u), __ll2double_rn(K));
+  if (MODE == M_FP32) {
+    float p = __fdiv_rn(__fadd_rn(__ll2float_rn(k), __double2float_rn(u)), __ll2float_rn(K));
+    return (double)p;
+  }
+  return __dmul_rn(__dadd_rn(__ll2double_rn(k), u), invK);
+}
+
+// ------------------------------------------------------------------------
+// fused frame kernel
+// ------------------------------------------------------------------------
+struct FusedArgs {
+  long long K;
+  int n_tiles;
+  int H, W, r, Wm;
+  int t;  // frame index in the stream (RNG position, t==0 -> identity ancestors)
+  const void* X_prev;
+  void* X_new;
+  const void* C_prev;
+  void* C_new;
+  const long long* tab_s;
+  const double* tab_O;
+  const double* tab_invM;
+  const double* u_prev;
+  const void* map;             // map of video 0 for this frame
+  long long map_video_stride;  // elements
+  int n_videos;
+  const unsigned long long* x0;
+  const ulonglong2* tj;  // f^(2 v VPT) per virtual thread v
+  double* rec_m;
+  long long* rec_S;
+  long long* rec_X;  // fp16: int64 moments; wide: double bits
+  long long* rec_Y;
+  const unsigned short* exp16;
+  double drift_x, drift_y, std_x, std_y;
+  long long* dbg_anc;  // optional
+  void* dbg_L;         // optional
+};
+
+template <typename T>
+__device__ __forceinline__ T shfl_up(T v, int d) {
+  return __shfl_up_sync(0xffffffffu, v, d);
+}
+
+template <typename T>
+__device__ __forceinline__ T block_excl_scan(T v, T* warp_buf, T* total) {
+  // inclusive warp scan
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  T x = v;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    T y = shfl_up(x, d);
+    if (lane >= d) x += y;
+  }
+  if (lane == 31) warp_buf[wid] = x;
+  __syncthreads();
+  if (wid == 0) {
+    T w = lane < nw ? warp_buf[lane] : (T)0;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      T y = shfl_up(w, d);
+      if (lane >= d) w += y;
+    }
+    if (lane < nw) warp_buf[lane] = w;  // inclusive warp prefix
+  }
+  __syncthreads();
+  T base = wid ? warp_buf[wid - 1] : (T)0;
+  *total = warp_buf[nw - 1];
+  __syncthreads();
+  return base + x - v;
+}
+
+template <int MODE>
+__device__ __forceinline__ typename Tr<MODE>::vec propagate_one(typename Tr<MODE>::vec xa, double n0, double n1,
+                                                                 const FusedArgs& a);
+
+template <>
+__device__ __forceinline__ double2 propagate_one<M_FP64>(double2 xa, double n0, double n1, const FusedArgs& a) {
+  double2 o;
+  o.x = __dadd_rn(__dadd_rn(xa.x, a.drift_x), __dmul_rn(a.std_x, n0));
+  o.y = __dadd_rn(__dadd_rn(xa.y, a.drift_y), __dmul_rn(a.std_y, n1));
+  return o;
+}
+template <>
+__device__ __forceinline__ float2 propagate_one<M_FP32>(float2 xa, double n0, double n1, const FusedArgs& a) {
+  float2 o;
+  o.x = __fadd_rn(__fadd_rn(xa.x, __double2float_rn(a.drift_x)),
+                  __fmul_rn(__double2float_rn(a.std_x), __double2float_rn(n0)));
+  o.y = __fadd_rn(__fadd_rn(xa.y, __double2float_rn(a.drift_y)),
+                  __fmul_rn(__double2float_rn(a.std_y), __double2float_rn(n1)));
+  return o;
+}
+template <>
+__device__ __forceinline__ __half2 propagate_one<M_FP16>(__half2 xa, double n0, double n1, const FusedArgs& a) {
+  // (x, y) travel in one half2: bx = x+drift, sx = std*n, x' = bx+sx (reference
+  // filter.py:362-379 semantics, each op RN16; _rn forbids HFMA contraction)
+  const __half2 drift = __halves2half2(__double2half(a.drift_x), __double2half(a.drift_y));
+  const __half2 stdv = __halves2half2(__double2half(a.std_x), __double2half(a.std_y));
+  const __half2 nn = __halves2half2(__double2half(n0), __double2half(n1));
+  return __hadd2_rn(__hadd2_rn(xa, drift), __hmul2_rn(stdv, nn));
+}
+
+template <int MODE>
+__device__ __forceinline__ int round_clamp(typename Tr<MODE>::real v, int lo, int hi);
+template <>
+__device__ __forceinline__ int round_clamp<M_FP64>(double v, int lo, int hi) {
+  return min(max(__double2int_rn(v), lo), hi);
+}
+template <>
+__device__ __forceinline__ int round_clamp<M_FP32>(float v, int lo, int hi) {
+  return min(max(__float2int_rn(v), lo), hi);
+}
+template <>
+__device__ __forceinline__ int round_clamp<M_FP16>(__half v, int lo, int hi) {
+  return min(max(__half2int_rn(v), lo), hi);
+}
+
+template <int MODE>
+__device__ __forceinline__ void vec_xy(typename Tr<MODE>::vec v, typename Tr<MODE>::real& x,
+                                       typename Tr<MODE>::real& y) {
+  x = v.x;
+  y = v.y;
+}
+
+template <typename real>
+__device__ __forceinline__ int lower_bound_c(const real* __restrict__ c, int lo, int hi, double q) {
+  while (lo < hi) {
+    int mid = (lo + hi) >> 1;
+    if (to_d(c[mid]) < q)
+      lo = mid + 1;
+    else
+      hi = mid;
+  }
+  return lo;
+}
+
+template <int MODE>
+__device__ __forceinline__ typename Tr<MODE>::real neg_inf();
+template <>
+__device__ __forceinline__ double neg_inf<M_FP64>() {
+  return __longlong_as_double(0xfff0000000000000LL);
+}
+template <>
+__device__ __forceinline__ float neg_inf<M_FP32>() {
+  return __int_as_float(0xff800000);
+}
+template <>
+__device__ __forceinline__ __half neg_inf<M_FP16>() {
+  return __ushort_as_half(0xfc00);
+}
+
+template <int MODE>
+__device__ __forceinline__ bool rgt(typename Tr<MODE>::real a, typename Tr<MODE>::real b) {
+  return to_d(a) > to_d(b);
+}
+
+// weight in fixed point: w_q = rint(exp(L - m) * 2^FB)
+template <int MODE>
+__device__ __forceinline__ typename Tr<MODE>::wq_t weight_q(typename Tr<MODE>::real L, typename Tr<MODE>::real m,
+                                                            const unsigned short* exp16);
+template <>
+__device__ __forceinline__ long long weight_q<M_FP64>(double L, double m, const unsigned short*) {
+  double w = pfm::exp64(__dsub_rn(L, m));
+  return __double2ll_rn(__dmul_rn(w, 4503599627370496.0));  // 2^52
+}
+template <>
+__device__ __forceinline__ long long weight_q<M_FP32>(float L, float m, const unsigned short*) {
+  float w = pfm::exp32(__fsub_rn(L, m));
+  return __float2ll_rn(__fmul_rn(w, 1099511627776.0f));  // 2^40
+}
+template <>
+__device__ __forceinline__ int weight_q<M_FP16>(__half L, __half m, const unsigned short* exp16) {
+  __half d = __hsub_rn(L, m);
+  __half w = __ushort_as_half(__ldg(exp16 + __half_as_ushort(d)));
+  return __float2int_rn(__fmul_rn(__half2float(w), 1048576.0f));  // 2^20
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(1024) pf_fused_frame(FusedArgs a) {
+  using real = typename Tr<MODE>::real;
+  using vec = typename Tr<MODE>::vec;
+  using wq_t = typename Tr<MODE>::wq_t;
+  constexpr int VPTMAX = 4;
+  extern __shared__ __align__(16) unsigned char smem[];
+  uint32_t* s_kihi = reinterpret_cast<uint32_t*>(smem);            // 1 KB
+  double* s_wi = reinterpret_cast<double*>(smem + 1024);           // 2 KB
+  real* s_L = reinterpret_cast<real*>(smem + 3072);                // TILE reals
+  vec* s_X = reinterpret_cast<vec*>(smem + 3072 + PF_TILE * sizeof(real));
+  unsigned char* s_misc = smem + 3072 + PF_TILE * (sizeof(real) + sizeof(vec));
+  long long* s_red = reinterpret_cast<long long*>(s_misc);         // 64 slots (scan / int moments)
+  double* s_redd = reinterpret_cast<double*>(s_misc + 64 * 8);     // 32 slots (max)
+  double* s_wx = reinterpret_cast<double*>(s_misc + 96 * 8);       // 32 slots
+  double* s_wy = reinterpret_cast<double*>(s_misc + 128 * 8);      // 32 slots
+  double* s_round = reinterpret_cast<double*>(s_misc + 160 * 8);   // 2 x 32 round values
+  unsigned long long* s_state = reinterpret_cast<unsigned long long*>(s_misc + 224 * 8);
+  double* s_mtile = reinterpret_cast<double*>(s_misc + 225 * 8);
+
+  const int TPB = blockDim.x;
+  const int VPT = TPB >= 1024 ? 1 : (TPB >= 512 ? 2 : VPTMAX);
+  const int R = PF_TILE / (TPB * VPT);
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, nw = TPB >> 5;
+  const int tile = blockIdx.x, track = blockIdx.y;
+  const long long K = a.K;
+  const long long base = (long long)tile * PF_TILE;
+  const int Tb = (int)min((long long)PF_TILE, K - base);
+
+  for (int i = tid; i < 256; i += TPB) {
+    s_kihi[i] = (uint32_t)(PF_ZIG_KI[i] >> 20);
+    s_wi[i] = __longlong_as_double((long long)PF_ZIG_WI_BITS[i]);
+  }
+  if (tid == 0) {
+    unsigned long long pos = (unsigned long long)a.t * (unsigned long long)(2 * K + 1) + 2ULL * (unsigned long long)base;
+    s_state[0] = pfr::word_at(a.x0[track], pos);
+  }
+  __syncthreads();
+  const unsigned long long tstate = s_state[0];
+
+  const vec* Xp = reinterpret_cast<const vec*>(a.X_prev) + (size_t)track * K;
+  vec* Xn = reinterpret_cast<vec*>(a.X_new) + (size_t)track * K;
+  const real* Cp = reinterpret_cast<const real*>(a.C_prev) + (size_t)track * K;
+  real* Cn = reinterpret_cast<real*>(a.C_new) + (size_t)track * K;
+  const real* map = reinterpret_cast<const real*>(a.map) + (size_t)(track % a.n_videos) * a.map_video_stride;
+  const long long* ts = a.tab_s + (size_t)track * a.n_tiles;
+  const double* tO = a.tab_O + (size_t)track * a.n_tiles;
+  const double* tM = a.tab_invM + (size_t)track * a.n_tiles;
+  const double u = a.t > 0 ? a.u_prev[track] : 0.0;
+  const double invK = __ddiv_rn(1.0, __ll2double_rn(K));
+  const int n = a.n_tiles;
+
+  // ---------------- phase 1: resample + propagate + likelihood ----------
+  real tmax = neg_inf<MODE>();
+  for (int rr = 0; rr < R; ++rr) {
+    const int v = rr * TPB + tid;  // virtual thread
+    const int l0 = v * VPT;        // local index of first particle
+    const long long k0 = base + l0;
+    unsigned long long xs = pfr::apply(pfr::Affine{a.tj[v].x, a.tj[v].y}, tstate);
+    long long anc[VPTMAX];
+    if (a.t == 0) {
+#pragma unroll
+      for (int i = 0; i < VPTMAX; ++i) anc[i] = k0 + i;
+    } else if (l0 < Tb) {
+      // source tile of the first particle: last b with s_b <= k0
+      int lo = 0, hi = n - 1;
+      while (lo < hi) {
+        int mid = (lo + hi + 1) >> 1;
+        if (__ldg(ts + mid) <= k0)
+          lo = mid;
+        else
+          hi = mid - 1;
+      }
+      int b = lo;
+      int jprev = 0, bprev = -1;
+#pragma unroll
+      for (int i = 0; i < VPTMAX; ++i) {
+        if (i >= VPT) break;
+        const long long k = k0 + i;
+        if (k >= K) {
+          anc[i] = 0;
+          continue;
+        }
+        while (b + 1 < n && __ldg(ts + b + 1) <= k) ++b;
+        const double p = point_of<MODE>(k, u, K, invK);
+        const double im = __ldg(tM + b);
+        double q = im == 0.0 ? 0.0 : __dmul_rn(__dsub_rn(p, __ldg(tO + b)), im);
+        q = fmin(fmax(q, 0.0), 1.0);
+        const long long tl = (long long)b * PF_TILE;
+        const int tb = (int)min((long long)PF_TILE, K - tl);
+        const int start = (b == bprev) ? jprev : 0;
+        int j = lower_bound_c<real>(Cp + tl, start, tb, q);
+        j = min(j, tb - 1);
+        jprev = j;
+        bprev = b;
+        anc[i] = tl + j;
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < VPTMAX; ++i) {
+      if (i >= VPT) break;
+      const int l = l0 + i;
+      const long long k = base + l;
+      const unsigned long long w0 = xs;
+      xs = pfr::kA * xs + pfr::kC;
+      const unsigned long long w1 = xs;
+      xs = pfr::kA * xs + pfr::kC;
+      if (l < Tb) {
+        const double n0 = pfr::normal_of(w0, s_kihi, s_wi);
+        const double n1 = pfr::normal_of(w1, s_kihi, s_wi);
+        const vec xa = Xp[anc[i]];
+        const vec xn = propagate_one<MODE>(xa, n0, n1, a);
+        Xn[k] = xn;
+        real px, py;
+        vec_xy<MODE>(xn, px, py);
+        const int ix = round_clamp<MODE>(px, -a.r, a.W - 1 + a.r);
+        const int iy = round_clamp<MODE>(py, -a.r, a.H - 1 + a.r);
+        const real L = map[(size_t)(iy + a.r) * a.Wm + (ix + a.r)];
+        s_L[l] = L;
+        s_X[l] = xn;
+        if (rgt<MODE>(L, tmax)) tmax = L;
+        if (a.dbg_anc) a.dbg_anc[(size_t)track * K + k] = anc[i];
+        if (a.dbg_L) reinterpret_cast<real*>(a.dbg_L)[(size_t)track * K + k] = L;
+      } else {
+        s_L[l] = neg_inf<MODE>();
+        vec z;
+        z.x = (real)0;
+        z.y = (real)0;
+        s_X[l] = z;
+      }
+    }
+  }
+  // tile max (exact: the max is one particle's L)
+  {
+    double m = to_d(tmax);
+#pragma unroll
+    for (int d = 16; d >= 1; d >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, d));
+    if (lane == 0) s_redd[wid] = m;
+    __syncthreads();
+    if (tid == 0) {
+      double mm = s_redd[0];
+      for (int w = 1; w < nw; ++w) mm = fmax(mm, s_redd[w]);
+      s_mtile[0] = mm;
+    }
+    __syncthreads();
+  }
+  const double mtile_d = s_mtile[0];
+  real mtile;
+  if constexpr (MODE == M_FP16)
+    mtile = __double2half(mtile_d);
+  else
+    mtile = (real)mtile_d;
+
+  // ---------------- phase 2: weights, exact scan, local cdf, moments ------
+  // cum_j is parked in the s_X slot of particle j/(sizeof(vec)/sizeof(wq_t))
+  // once that position has been consumed (rounds advance monotonically).
+  wq_t carry = 0;
+  long long mx_i = 0, my_i = 0;  // fp16 moments (exact)
+  for (int rr = 0; rr < R; ++rr) {
+    const int v = rr * TPB + tid;
+    const int l0 = v * VPT;
+    wq_t wq[VPTMAX];
+    wq_t loc = 0;
+#pragma unroll
+    for (int i = 0; i < VPTMAX; ++i) {
+      if (i >= VPT) break;
+      const int l = l0 + i;
+      wq[i] = (l < Tb) ? weight_q<MODE>(s_L[l], mtile, a.exp16) : (wq_t)0;
+      loc += wq[i];
+    }
+    wq_t tot;
+    const wq_t excl = block_excl_scan<wq_t>(loc, reinterpret_cast<wq_t*>(s_red), &tot);
+    double px_d[VPTMAX], py_d[VPTMAX];
+#pragma unroll
+    for (int i = 0; i < VPTMAX; ++i) {
+      if (i >= VPT) break;
+      const vec xv = s_X[l0 + i];
+      if constexpr (MODE == M_FP16) {
+        const int xq = __float2int_rn(__fmul_rn(__half2float(xv.x), 1024.0f));
+        const int yq = __float2int_rn(__fmul_rn(__half2float(xv.y), 1024.0f));
+        mx_i += (long long)wq[i] * xq;
+        my_i += (long long)wq[i] * yq;
+      } else {
+        const double wd = (double)wq[i];
+        px_d[i] = __dmul_rn(wd, to_d(xv.x));
+        py_d[i] = __dmul_rn(wd, to_d(xv.y));
+      }
+    }
+    wq_t run = carry + excl;
+#pragma unroll
+    for (int i = 0; i < VPTMAX; ++i) {
+      if (i >= VPT) break;
+      run += wq[i];
+      wq[i] = run;  // inclusive cum
+    }
+    __syncthreads();  // every position of this round has been read
+#pragma unroll
+    for (int i = 0; i < VPTMAX; ++i) {
+      if (i >= VPT) break;
+      reinterpret_cast<wq_t*>(s_X)[l0 + i] = wq[i];
+    }
+    carry += tot;
+    if constexpr (MODE != M_FP16) {
+      // canonical pairwise tree: VPT-local, lane butterfly, warps, rounds
+      double sx, sy;
+      if (VPT == 4) {
+        sx = __dadd_rn(__dadd_rn(px_d[0], px_d[1]), __dadd_rn(px_d[2], px_d[3]));
+        sy = __dadd_rn(__dadd_rn(py_d[0], py_d[1]), __dadd_rn(py_d[2], py_d[3]));
+      } else if (VPT == 2) {
+        sx = __dadd_rn(px_d[0], px_d[1]);
+        sy = __dadd_rn(py_d[0], py_d[1]);
+      } else {
+        sx = px_d[0];
+        sy = py_d[0];
+      }
+#pragma unroll
+      for (int d = 1; d < 32; d <<= 1) {
+        sx = __dadd_rn(sx, __shfl_xor_sync(0xffffffffu, sx, d));
+        sy = __dadd_rn(sy, __shfl_xor_sync(0xffffffffu, sy, d));
+      }
+      if (lane == 0) {
+        s_wx[wid] = sx;
+        s_wy[wid] = sy;
+      }
+      __syncthreads();
+      if (tid == 0) {
+        for (int width = nw; width > 1; width >>= 1)
+          for (int w = 0; w < width / 2; ++w) {
+            s_wx[w] = __dadd_rn(s_wx[2 * w], s_wx[2 * w + 1]);
+            s_wy[w] = __dadd_rn(s_wy[2 * w], s_wy[2 * w + 1]);
+          }
+        s_round[rr] = s_wx[0];
+        s_round[32 + rr] = s_wy[0];
+      }
+      __syncthreads();
+    }
+  }
+  const wq_t S = carry;
+  __syncthreads();
+  // local cdf c_j = d(cum_j / S), forced to 1 where cum_j == S
+  if constexpr (MODE == M_FP16) {
+    const float invf = __fdiv_rn(1.0f, (float)S);
+    for (int l = tid; l < Tb; l += TPB) {
+      const int cum = reinterpret_cast<const int*>(s_X)[l];
+      Cn[base + l] = (cum == S) ? __float2half(1.0f) : __float2half_rn(__fmul_rn((float)cum, invf));
+    }
+  } else {
+    const double inv = __ddiv_rn(1.0, (double)S);
+    for (int l = tid; l < Tb; l += TPB) {
+      const long long cum = reinterpret_cast<const long long*>(s_X)[l];
+      const double cd = __dmul_rn((double)cum, inv);
+      if constexpr (MODE == M_FP32)
+        Cn[base + l] = (cum == S) ? 1.0f : __double2float_rn(cd);
+      else
+        Cn[base + l] = (cum == S) ? 1.0 : cd;
+    }
+  }
+  // tile record
+  const size_t ri = (size_t)track * n + tile;
+  if constexpr (MODE == M_FP16) {
+#pragma unroll
+    for (int d = 16; d >= 1; d >>= 1) {
+      mx_i += __shfl_xor_sync(0xffffffffu, mx_i, d);
+      my_i += __shfl_xor_sync(0xffffffffu, my_i, d);
+    }
+    if (lane == 0) {
+      s_red[wid] = mx_i;
+      s_red[32 + wid] = my_i;
+    }
+    __syncthreads();
+    if (tid == 0) {
+      long long sx = 0, sy = 0;
+      for (int w = 0; w < nw; ++w) {
+        sx += s_red[w];
+        sy += s_red[32 + w];
+      }
+      a.rec_m[ri] = mtile_d;
+      a.rec_S[ri] = (long long)S;
+      a.rec_X[ri] = sx;
+      a.rec_Y[ri] = sy;
+    }
+  } else {
+    if (tid == 0) {
+      for (int width = R; width > 1; width >>= 1)
+        for (int w = 0; w < width / 2; ++w) {
+          s_round[w] = __dadd_rn(s_round[2 * w], s_round[2 * w + 1]);
+          s_round[32 + w] = __dadd_rn(s_round[32 + 2 * w], s_round[32 + 2 * w + 1]);
+        }
+      a.rec_m[ri] = mtile_d;
+      a.rec_S[ri] = (long long)S;
+      a.rec_X[ri] = __double_as_longlong(s_round[0]);
+      a.rec_Y[ri] = __double_as_longlong(s_round[32]);
+    }
+  }
+}
+
+// ------------------------------------------------------------------------
+// tile table (one CTA per track)
+// ------------------------------------------------------------------------
+struct TableArgs {
+  long long K;
+  int n_tiles, n_pad;
+  int t;
+  int Q;
+  const unsigned long long* x0;
+  const double* rec_m;
+  const long long* rec_S;
+  const long long* rec_X;
+  const long long* rec_Y;
+  long long* tab_s;
+  double* tab_O;
+  double* tab_invM;
+  double* u_out;
+  double* traj;       // [track][F][2]
+  int traj_stride;    // frames per track in traj
+  int traj_index;     // frame slot
+  int* degenerate;    // per track: first degenerate frame (or INT_MAX)
+};
+
+// canonical pairwise accumulation over a power-of-two run (binary counter)
+struct PwAcc {
+  double st[24];
+  int i;
+  __device__ void reset() { i = 0; }
+  __device__ void push(double v) {
+    int j = i, lvl = 0;
+    while (j & 1) {
+      v = __dadd_rn(st[lvl], v);
+      j >>= 1;
+      ++lvl;
+    }
+    st[lvl] = v;
+    ++i;
+  }
+  __device__ double root() const {  // i is a power of two
+    int lvl = 0;
+    while ((1 << lvl) < i) ++lvl;
+    return st[lvl];
+  }
+};
+
+template <int MODE>
+__global__ void __launch_bounds__(1024) pf_tile_table(TableArgs a) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  long long* s_i = reinterpret_cast<long long*>(smem);     // 32
+  double* s_d = reinterpret_cast<double*>(smem + 32 * 8);  // 3 x 32 + 2
+  constexpr int FB = Tr<MODE>::FB;
+  const int track = blockIdx.x, tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const int TPB = blockDim.x, nw = TPB >> 5;
+  const int n = a.n_tiles;
+  const int Rt = max(1, a.n_pad / TPB);  // tiles per thread (power of two)
+  const int b0 = tid * Rt;
+  const double* rm = a.rec_m + (size_t)track * n;
+  const long long* rS = a.rec_S + (size_t)track * n;
+  const long long* rX = a.rec_X + (size_t)track * n;
+  const long long* rY = a.rec_Y + (size_t)track * n;
+
+  // 1. global max (exact) + the frame's resampling uniform
+  double m = __longlong_as_double(0xfff0000000000000LL);
+  for (int i = 0; i < Rt; ++i)
+    if (b0 + i < n) m = fmax(m, rm[b0 + i]);
+#pragma unroll
+  for (int d = 16; d >= 1; d >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, d));
+  if (lane == 0) s_d[wid] = m;
+  __syncthreads();
+  if (tid == 0) {
+    double mm = s_d[0];
+    for (int w = 1; w < nw; ++w) mm = fmax(mm, s_d[w]);
+    s_d[96] = mm;
+    const unsigned long long pos =
+        (unsigned long long)a.t * (unsigned long long)(2 * a.K + 1) + 2ULL * (unsigned long long)a.K;
+    s_d[97] = pfr::uniform_of(pfr::word_at(a.x0[track], pos));
+  }
+  __syncthreads();
+  m = s_d[96];
+  const double u = s_d[97];
+  __syncthreads();
+  const double scale = ldexp(1.0, a.Q - FB);
+
+  // 2. exact fixed-point tile masses and their prefix
+  long long loc = 0;
+  for (int i = 0; i < Rt; ++i) {
+    const int b = b0 + i;
+    if (b < n) {
+      const double f = pfm::exp64(__dsub_rn(rm[b], m));
+      loc += __double2ll_rn(__dmul_rn(__dmul_rn((double)rS[b], f), scale));
+    }
+  }
+  long long tot;
+  const long long excl = block_excl_scan<long long>(loc, s_i, &tot);
+  const double Sq = (double)tot;
+  const double invK = __ddiv_rn(1.0, __ll2double_rn(a.K));
+
+  // 3. table entries + estimate moments (canonical tree over padded tiles)
+  long long run = excl;
+  PwAcc ax, ay, ad;
+  ax.reset();
+  ay.reset();
+  ad.reset();
+  for (int i = 0; i < Rt; ++i) {
+    const int b = b0 + i;
+    double vx = 0.0, vy = 0.0, vd = 0.0;
+    if (b < n) {
+      const double f = pfm::exp64(__dsub_rn(rm[b], m));
+      const long long mass = __double2ll_rn(__dmul_rn(__dmul_rn((double)rS[b], f), scale));
+      const double O = __ddiv_rn((double)run, Sq);
+      const double invM = mass > 0 ? __ddiv_rn(Sq, (double)mass) : 0.0;
+      long long s = 0;
+      if (b > 0) {
+        long long k = (long long)floor(__dsub_rn(__dmul_rn(O, (double)a.K), u));
+        k = min(max(k, 0LL), a.K);
+        while (k > 0 && point_of<MODE>(k - 1, u, a.K, invK) > O) --k;
+        while (k < a.K && point_of<MODE>(k, u, a.K, invK) <= O) ++k;
+        s = k;
+      }
+      const size_t ti = (size_t)track * n + b;
+      a.tab_s[ti] = s;
+      a.tab_O[ti] = O;
+      a.tab_invM[ti] = invM;
+      double X, Y;
+      if constexpr (MODE == M_FP16) {
+        X = (double)rX[b];
+        Y = (double)rY[b];
+      } else {
+        X = __longlong_as_double(rX[b]);
+        Y = __longlong_as_double(rY[b]);
+      }
+      vx = __dmul_rn(f, X);
+      vy = __dmul_rn(f, Y);
+      vd = __dmul_rn(f, (double)rS[b]);
+      run += mass;
+    }
+    ax.push(vx);
+    ay.push(vy);
+    ad.push(vd);
+  }
+  double nx = ax.root(), ny = ay.root(), den = ad.root();
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    nx = __dadd_rn(nx, __shfl_xor_sync(0xffffffffu, nx, d));
+    ny = __dadd_rn(ny, __shfl_xor_sync(0xffffffffu, ny, d));
+    den = __dadd_rn(den, __shfl_xor_sync(0xffffffffu, den, d));
+  }
+  if (lane == 0) {
+    s_d[wid] = nx;
+    s_d[32 + wid] = ny;
+    s_d[64 + wid] = den;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    for (int width = nw; width > 1; width >>= 1)
+      for (int w = 0; w < width / 2; ++w) {
+        s_d[w] = __dadd_rn(s_d[2 * w], s_d[2 * w + 1]);
+        s_d[32 + w] = __dadd_rn(s_d[32 + 2 * w], s_d[32 + 2 * w + 1]);
+        s_d[64 + w] = __dadd_rn(s_d[64 + 2 * w], s_d[64 + 2 * w + 1]);
+      }
+    const double D = s_d[64];
+    double ex = __ddiv_rn(s_d[0], D);
+    double ey = __ddiv_rn(s_d[32], D);
+    if constexpr (MODE == M_FP16) {
+      ex = __dmul_rn(ex, 1.0 / 1024.0);
+      ey = __dmul_rn(ey, 1.0 / 1024.0);
+    }
+    double* tr = a.traj + ((size_t)track * a.traj_stride + a.traj_index) * 2;
+    tr[0] = ex;
+    tr[1] = ey;
+    a.u_out[track] = u;
+    if (!(D > 0.0) || !isfinite(D) || !isfinite(ex) || !isfinite(ey)) atomicMin(a.degenerate + track, a.t);
+  }
+}
+
+}  // namespace pfk
