@@ -1,0 +1,439 @@
+#!/usr/bin/env python
+"""bench.py -- particle-updates/s of the fused per-frame tracking step on B200.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2] [--impl reference]
+
+A "step" is one full tracking run over the config's synthetic video (every
+frame: resample -> propagate -> likelihood -> weights -> exact scan / local
+CDF -> estimate, plus the per-frame likelihood maps), i.e. K*F particle-
+updates per track.  Default config C2 (BASELINE.json configs[1]): 128x128,
+100 frames, 1M particles, stabilised FP16 (FP32 / FP64 measured alongside).
+With N GPUs (torchrun) every rank runs its own independent track(s) -- the
+batched-track sharding of the north star, no collective on the data path
+(weak scaling).  Timing: device CUDA events recorded by the library on its
+own stream, L2 flushed (512 MiB write) before every timed step, max over
+ranks.  `e2e` re-times the same steps through the host-buffer C-ABI call
+(frames H2D + trajectory D2H inside the region, wall clock).
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import platform
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "particle-updates/sec (N×frames/s) fp16/fp32/fp64 at 1–8 B200; tracking RMSE"
+UNIT = "particle-updates/s"
+SIZES = {"fp64": 8, "fp32": 4, "fp16": 2, "fp16-packed": 2}
+DTYPE_TAG = {"fp64": "f64", "fp32": "f32", "fp16": "f16", "fp16-packed": "f16"}
+
+CONFIGS = {
+    "c1": dict(W=128, H=128, F=10, K=10_000, precision="fp64", tracks=1, videos=1,
+               desc="C1: 128x128 video, 10 frames, 10,000 particles, FP64"),
+    "c2": dict(W=128, H=128, F=100, K=1_000_000, precision="fp16", tracks=1, videos=1,
+               desc="C2: 128x128 video, 100 frames, 1M particles, stabilised FP16 (FP32/FP64 alongside)"),
+    "c3": dict(W=1024, H=1024, F=100, K=1 << 24, precision="fp16", tracks=1, videos=1,
+               desc="C3: 1024x1024 video, 100 frames, 16M particles, FP16 half2"),
+    "c4": dict(W=128, H=128, F=100, K=65536, precision="fp16", tracks=8192, videos=8,
+               desc="C4: 8192 independent 128x128 tracks x 64K particles, FP16 (tracks split over GPUs)"),
+}
+
+
+def _peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            p = json.load(fh)
+        return float(p["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, copy)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device_index: int):
+        self.dev = device_index
+        self.rows = []
+        self.proc = None
+        self.thread = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.dev), f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+            return
+        self.thread = threading.Thread(target=self._read, daemon=True)
+        self.thread.start()
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 9:
+                self.rows.append(parts)
+
+    def stop(self):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+        if self.thread is not None:
+            self.thread.join(timeout=2)
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        sm, mx, reasons = [], [], set()
+        for r in self.rows:
+            try:
+                sm.append(float(r[1]))
+                mx.append(float(r[2]))
+            except ValueError:
+                continue
+            for n, v in zip(names, r[5:9]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------
+# CPU reference arm (oracle port of the reference algorithm; test infrastructure)
+# ---------------------------------------------------------------------------
+
+
+def _cpu_worker(conn, K, frames, seed, mode):
+    from oracle import reference_port as rp
+    from oracle import rng
+
+    eng = rp.make_engine(mode, rp.Params(), rp.disk_offsets(5), direct=True)
+    H, W = frames.shape[1:]
+    s = eng.init(K, (W / 2.0, H / 2.0))
+    stream = rng.LcgStream(seed)
+    t = 0
+    while True:
+        msg = conn.recv()
+        if msg is None:
+            break
+        nf = msg
+        t0 = time.perf_counter()
+        for _ in range(nf):
+            eng.propagate(s, stream.normals(K))
+            eng.likelihoods(s, frames[t % len(frames)])
+            m = eng.max_loglik(s)
+            tot = eng.weight_update(s, m)
+            eng.normalize_and_scan(s, tot)
+            eng.estimate(s)
+            eng.resample(s, stream.uniform())
+            t += 1
+        conn.send(time.perf_counter() - t0)
+
+
+class CpuArm:
+    """P worker processes, each one independent track of the oracle port
+    (restatement of halfpf's wide engine, filter.py:172-255, with the
+    reference's direct (K, N) likelihood gather)."""
+
+    def __init__(self, K, frames, mode, procs):
+        import multiprocessing as mp
+
+        ctx = mp.get_context("fork")
+        self.procs = []
+        for i in range(procs):
+            a, b = ctx.Pipe()
+            p = ctx.Process(target=_cpu_worker, args=(b, K, frames, 1000 + i, mode), daemon=True)
+            p.start()
+            self.procs.append((p, a))
+
+    def step(self, frames_per_worker):
+        t0 = time.perf_counter()
+        for _, c in self.procs:
+            c.send(frames_per_worker)
+        for _, c in self.procs:
+            c.recv()
+        return time.perf_counter() - t0
+
+    def close(self):
+        for p, c in self.procs:
+            try:
+                c.send(None)
+            except Exception:
+                pass
+            p.join(timeout=5)
+
+
+def cpu_sample(cfg, mode="fp32", procs=1, frames=2, K=None):
+    from oracle import reference_port as rp
+
+    K = K or min(cfg["K"], 1_000_000)
+    vid, _ = rp.generate_video(rp.Params(), max(frames, 2), cfg["W"], cfg["H"],
+                               (cfg["W"] / 2.0, cfg["H"] / 2.0), 42)
+    arm = CpuArm(K, vid, mode, procs)
+    try:
+        arm.step(1)  # warm (allocations, page faults)
+        dt = arm.step(frames)
+    finally:
+        arm.close()
+    return procs * K * frames / dt, dict(K=K, frames=frames, mode=mode, seconds=dt)
+
+
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return platform.processor()
+
+
+def run_reference_arm(args, cfg, rank, world):
+    if rank != 0:
+        return
+    procs = len(os.sched_getaffinity(0))
+    from oracle import reference_port as rp
+
+    K = min(cfg["K"], 1_000_000)
+    vid, _ = rp.generate_video(rp.Params(), 4, cfg["W"], cfg["H"], (cfg["W"] / 2.0, cfg["H"] / 2.0), 42)
+    mode = "fp32" if cfg["precision"].startswith("fp16") else cfg["precision"]
+    arm = CpuArm(K, vid, mode, procs)
+    try:
+        for _ in range(args.warmup):
+            arm.step(1)
+        times = [arm.step(1) for _ in range(args.steps)]
+    finally:
+        arm.close()
+    tot = sum(times)
+    value = procs * K * args.steps / tot
+    sample = (f"oracle port of halfpf {mode} wide engine (direct (K,81) gather, NumPy, 1 thread/process), "
+              f"{procs} processes x 1 frame of {K} particles per step on {cfg['W']}x{cfg['H']}; "
+              f"reference FP16 is pure-Python emulation, degenerate at K>=65536, so FP32 is the CPU arm")
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": DTYPE_TAG[mode],
+        "data": "synthetic", "config": _config_block(cfg, args),
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": procs, "kind": "port", "sample": sample,
+                         "cpu": cpu_model()},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def _config_block(cfg, args):
+    return {"workload": cfg["desc"], "width": cfg["W"], "height": cfg["H"], "frames": cfg["F"],
+            "particles_per_track": cfg["K"], "tracks": cfg["tracks"], "precision": cfg["precision"],
+            "tpb": args.tpb, "l2": "flushed (512 MiB write) before every timed step",
+            "rng": "counter-based LCG (device)", "parallelism": f"tracks/GPU, {args.gpus} GPU(s), no collective"}
+
+
+# ---------------------------------------------------------------------------
+# GPU arm
+# ---------------------------------------------------------------------------
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
+    ap.add_argument("--precision", default=None)
+    ap.add_argument("--tpb", type=int, default=256)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-extra", action="store_true", help="skip the FP32/FP64 side measurements")
+    ap.add_argument("--profile-only", action="store_true", help="(ncu) run 1 untimed step, no JSON")
+    args = ap.parse_args()
+    cfg = dict(CONFIGS[args.config])
+    if args.precision:
+        cfg["precision"] = args.precision
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference_arm(args, cfg, rank, world)
+        return
+
+    import torch
+
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    import paper_2308_00763_b200 as pf
+
+    tracks = max(1, cfg["tracks"] // world) if cfg["tracks"] > 1 else 1
+    F, K, W, H = cfg["F"], cfg["K"], cfg["W"], cfg["H"]
+    nv = cfg["videos"]
+    vids, truths = [], []
+    for j in range(nv):
+        v = pf.generate_video(pf.ModelParams(), F, W, H, (W / 2.0, H / 2.0), 42 + j)
+        vids.append(v.frames)
+        truths.append(v.truth)
+    host_frames = np.ascontiguousarray(np.stack(vids)) if nv > 1 else vids[0]
+    dev_frames = torch.from_numpy(host_frames).cuda()
+    flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
+    seeds = [42 + rank * tracks + i for i in range(tracks)]
+
+    def make(precision):
+        return pf.Filter(K, precision, W, H, seeds=seeds, n_tracks=tracks, n_videos=nv, tpb=args.tpb,
+                         device=local)
+
+    def device_steps(f, n, timed=True):
+        tot = 0.0
+        launches = 0
+        for _ in range(n):
+            flush.zero_()
+            torch.cuda.synchronize()
+            f.reset()
+            f.run_frames(dev_frames, F)
+            tot += f.timings()["total"]
+            launches += f.launches()
+        return tot, launches
+
+    def barrier():
+        torch.cuda.synchronize()
+        if dist is not None:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def max_over_ranks(x):
+        if dist is None:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    prec = cfg["precision"]
+    f = make(prec)
+    if args.profile_only:
+        f.run_frames(dev_frames, F)
+        torch.cuda.synchronize()
+        return
+    device_steps(f, args.warmup)
+    clocks = ClockSampler(local)
+    barrier()
+    clocks.start()
+    dev_ms, launches = device_steps(f, args.steps)
+    barrier()
+    clk = clocks.stop()
+    dev_ms = max_over_ranks(dev_ms)
+    updates_per_step = world * tracks * K * F
+    value = updates_per_step * args.steps / (dev_ms * 1e-3)
+    traj = f.run_frames(dev_frames, F)
+    truth = truths[0]
+    rmse, mean_err, max_err = pf.accuracy_metrics(traj[0], truth)
+
+    # ---- e2e through the host-buffer C-ABI call (H2D + D2H inside) --------
+    barrier()
+    e2e_s = 0.0
+    for _ in range(args.steps):
+        flush.zero_()
+        torch.cuda.synchronize()
+        f.reset()
+        t0 = time.perf_counter()
+        f.run_frames(host_frames, F)
+        e2e_s += time.perf_counter() - t0
+    barrier()
+    e2e_s = max_over_ranks(e2e_s)
+    e2e = {"value": updates_per_step * args.steps / e2e_s, "unit": UNIT,
+           "h2d_bytes_per_step": int(host_frames.nbytes), "d2h_bytes_per_step": int(tracks * F * 2 * 8),
+           "ms_per_step": 1e3 * e2e_s / args.steps, "timer": "wall clock around pf_run (host frames)"}
+
+    # ---- roofline of the dominant kernel (fused frame kernel) ------------
+    f.set_profiling(True)
+    flush.zero_()
+    torch.cuda.synchronize()
+    f.reset()
+    f.run_frames(dev_frames, F)
+    tm = f.timings()
+    f.set_profiling(False)
+    s = SIZES[prec]
+    fused_avg_ms = tm["frames"] / F
+    table_avg_ms = tm["tables"] / F
+    bytes_per_launch = tracks * K * 6 * s + nv * W * H
+    peak, peak_src = _peaks()
+    achieved = bytes_per_launch / (fused_avg_ms * 1e-3) / 1e9
+    traffic = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as fh:
+            tr = json.load(fh).get(f"{args.config}_{prec}")
+            if tr:
+                traffic = tr["dram_bytes_per_launch"]
+    except Exception:
+        pass
+    roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                "traffic": traffic, "kernel": f"pf_fused_frame<{prec}>",
+                "algorithmic_bytes_per_launch": bytes_per_launch,
+                "bytes_per_particle": 6 * s, "avg_launch_ms": fused_avg_ms, "tile_table_avg_ms": table_avg_ms,
+                "maps_ms_per_step": tm["maps"], "peak_source": peak_src}
+    f.close()
+
+    # ---- the other precisions of the same workload -----------------------
+    extra = {}
+    if not args.no_extra and args.config == "c2":
+        for p2 in ("fp32", "fp64"):
+            g = make(p2)
+            device_steps(g, 2)
+            ms2, _ = device_steps(g, max(3, args.steps // 2))
+            ms2 = max_over_ranks(ms2)
+            v2 = updates_per_step * max(3, args.steps // 2) / (ms2 * 1e-3)
+            t2 = g.run_frames(dev_frames, F)
+            e2 = pf.accuracy_metrics(t2[0], truth)
+            extra[p2] = {"value": v2, "unit": UNIT, "tracking_rmse_px": e2[0], "tracking_mean_err_px": e2[1]}
+            g.close()
+        extra[prec] = {"value": value, "unit": UNIT, "tracking_rmse_px": rmse, "tracking_mean_err_px": mean_err}
+        extra["fp16_over_fp32"] = value / extra["fp32"]["value"]
+        extra["fp16_over_fp64"] = value / extra["fp64"]["value"]
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        mode = "fp32" if prec.startswith("fp16") else prec
+        rate, info = cpu_sample(cfg, mode=mode, procs=1, frames=2)
+        cpu = {"value": rate, "unit": UNIT, "cores": 1, "kind": "port",
+               "sample": (f"oracle port of halfpf {mode} wide engine (direct (K,81) gather), {info['frames']} frames "
+                          f"of {info['K']} particles on the C2 video ({info['seconds']:.1f} s); reference FP16 is "
+                          f"pure-Python emulation and degenerate at K>=65536"),
+               "cpu": cpu_model()}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": dev_ms / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": DTYPE_TAG[prec], "data": "synthetic",
+            "config": _config_block(cfg, args),
+            "e2e": e2e, "roofline": roofline, "cpu_baseline": cpu, "clocks": clk,
+            "gpu_launches": launches,
+            "tracking": {"rmse_px": rmse, "mean_err_px": mean_err, "max_err_px": max_err},
+            "by_precision": extra or None,
+        }
+        print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

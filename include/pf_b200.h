@@ -96,6 +96,11 @@ int pf_degenerate_frame(const pf_handle* h);
  * [4] tile tables, [5] download. */
 int pf_last_timings(const pf_handle* h, float* ms6);
 
+/* Per-kernel event timing: when on, timings [3]/[4] of the next runs are the
+ * summed durations of the fused frame kernels / tile-table kernels alone
+ * (events between launches on the handle's stream). */
+int pf_set_profiling(pf_handle* h, int32_t on);
+
 /* Kernel launches issued by the last pf_run/pf_step. */
 int64_t pf_last_launches(const pf_handle* h);
 

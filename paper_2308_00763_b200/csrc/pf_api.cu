@@ -164,6 +164,8 @@ struct pf_handle {
   int degenerate_frame = -1;
   size_t map_smem = 0, fused_smem = 0;
   int map_band = 32;
+  bool profiling = false;
+  std::vector<cudaEvent_t> pev;  // 3 per frame when profiling
 };
 
 static int grow(void** p, size_t* cap, size_t bytes, std::string& err) {
@@ -198,6 +200,7 @@ int pf_destroy(pf_handle* h) {
     if (p) cudaFree(p);
   for (auto& e : h->ev)
     if (e) cudaEventDestroy(e);
+  for (auto& e : h->pev) cudaEventDestroy(e);
   if (h->stream) cudaStreamDestroy(h->stream);
   delete h;
   return PF_OK;
@@ -426,6 +429,7 @@ static int launch_maps(pf_handle* h, const uint8_t* dframes, int F) {
 // one frame: fused kernel + tile table
 static int launch_frame(pf_handle* h, const void* map_slot, long long map_video_stride, int traj_index,
                         int traj_stride) {
+  if (h->profiling) PF_CUDA(cudaEventRecord(h->pev[3 * traj_index + 0], h->stream), h->err);
   pfk::FusedArgs a{};
   a.K = h->K;
   a.n_tiles = h->n_tiles;
@@ -466,6 +470,7 @@ static int launch_frame(pf_handle* h, const void* map_slot, long long map_video_
   else
     pfk::pf_fused_frame<2><<<grid, h->tpb, h->fused_smem, h->stream>>>(a);
   PF_CUDA(cudaGetLastError(), h->err);
+  if (h->profiling) PF_CUDA(cudaEventRecord(h->pev[3 * traj_index + 1], h->stream), h->err);
   pfk::TableArgs t{};
   t.K = h->K;
   t.n_tiles = h->n_tiles;
@@ -493,6 +498,7 @@ static int launch_frame(pf_handle* h, const void* map_slot, long long map_video_
   else
     pfk::pf_tile_table<2><<<h->n_tracks, h->tpb_table, tsm, h->stream>>>(t);
   PF_CUDA(cudaGetLastError(), h->err);
+  if (h->profiling) PF_CUDA(cudaEventRecord(h->pev[3 * traj_index + 2], h->stream), h->err);
   h->launches += 2;
   h->cur = 1 - h->cur;
   h->frame_counter += 1;
@@ -521,6 +527,13 @@ int pf_run(pf_handle* h, const uint8_t* frames, int32_t F, int32_t on_device, do
   int rc;
   if ((rc = grow((void**)&h->d_maps, &h->maps_cap, (size_t)h->n_videos * F * map_elems * h->rs, h->err))) return rc;
   if ((rc = grow((void**)&h->d_traj, &h->traj_cap, (size_t)h->n_tracks * F * 2 * 8, h->err))) return rc;
+  if (h->profiling) {
+    while ((int)h->pev.size() < 3 * F) {
+      cudaEvent_t e;
+      PF_CUDA(cudaEventCreate(&e), h->err);
+      h->pev.push_back(e);
+    }
+  }
   const uint8_t* dframes = frames;
   if (!on_device) {
     if ((rc = grow((void**)&h->d_frames, &h->frames_cap, fbytes, h->err))) return rc;
@@ -552,6 +565,17 @@ int pf_run(pf_handle* h, const uint8_t* frames, int32_t F, int32_t on_device, do
   cudaEventElapsedTime(&ms, h->ev[2], h->ev[3]);
   h->timings[3] = ms;
   h->timings[4] = 0.f;
+  if (h->profiling) {
+    float fsum = 0.f, tsum = 0.f;
+    for (int f = 0; f < F; ++f) {
+      cudaEventElapsedTime(&ms, h->pev[3 * f], h->pev[3 * f + 1]);
+      fsum += ms;
+      cudaEventElapsedTime(&ms, h->pev[3 * f + 1], h->pev[3 * f + 2]);
+      tsum += ms;
+    }
+    h->timings[3] = fsum;
+    h->timings[4] = tsum;
+  }
   cudaEventElapsedTime(&ms, h->ev[3], h->ev[4]);
   h->timings[5] = ms;
   return finish_degenerate(h);
@@ -562,6 +586,12 @@ int pf_step(pf_handle* h, const uint8_t* frame, int32_t on_device, double* est_o
 }
 
 int pf_degenerate_frame(const pf_handle* h) { return h ? h->degenerate_frame : -1; }
+
+int pf_set_profiling(pf_handle* h, int32_t on) {
+  if (!h) return PF_EINVAL;
+  h->profiling = on != 0;
+  return PF_OK;
+}
 
 int pf_last_timings(const pf_handle* h, float* ms6) {
   if (!h || !ms6) return PF_EINVAL;

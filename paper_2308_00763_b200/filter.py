@@ -439,6 +439,9 @@ class Filter:
         keys = ("total", "upload", "maps", "frames", "tables", "download")
         return {k: float(v) for k, v in zip(keys, t)}
 
+    def set_profiling(self, on: bool = True):
+        N.check(N.lib().pf_set_profiling(self._h, int(bool(on))), self._err)
+
     def launches(self) -> int:
         return int(N.lib().pf_last_launches(self._h))
 
