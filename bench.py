@@ -61,59 +61,51 @@ def _peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
-
-    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
-         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    """SM clocks + throttle reasons sampled (NVML, every 10 ms) during the timed region."""
 
     def __init__(self, device_index: int):
         self.dev = device_index
         self.rows = []
-        self.proc = None
+        self._stop = threading.Event()
         self.thread = None
 
     def start(self):
         try:
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", "-i", str(self.dev), f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
-                 "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            import pynvml as nv
+
+            nv.nvmlInit()
+            h = nv.nvmlDeviceGetHandleByIndex(self.dev)
+            self.mx = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
         except Exception:
-            self.proc = None
+            self.thread = None
             return
-        self.thread = threading.Thread(target=self._read, daemon=True)
+
+        def loop():
+            bits = {"hw_slowdown": 0x8, "hw_thermal_slowdown": 0x40, "sw_thermal_slowdown": 0x20,
+                    "sw_power_cap": 0x4, "hw_power_brake_slowdown": 0x80}
+            while not self._stop.is_set():
+                try:
+                    clk = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
+                    r = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+                    self.rows.append((clk, [n for n, b in bits.items() if r & b]))
+                except Exception:
+                    pass
+                time.sleep(0.01)
+
+        self.thread = threading.Thread(target=loop, daemon=True)
         self.thread.start()
 
-    def _read(self):
-        for line in self.proc.stdout:
-            parts = [p.strip() for p in line.split(",")]
-            if len(parts) >= 9:
-                self.rows.append(parts)
-
     def stop(self):
-        if self.proc is not None:
-            self.proc.terminate()
-            try:
-                self.proc.wait(timeout=5)
-            except Exception:
-                self.proc.kill()
-        if self.thread is not None:
-            self.thread.join(timeout=2)
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        sm, mx, reasons = [], [], set()
-        for r in self.rows:
-            try:
-                sm.append(float(r[1]))
-                mx.append(float(r[2]))
-            except ValueError:
-                continue
-            for n, v in zip(names, r[5:9]):
-                if v.lower() == "active":
-                    reasons.add(n)
-        if not sm:
+        if self.thread is None:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
-        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
-                "samples": len(sm)}
+        self._stop.set()
+        self.thread.join(timeout=2)
+        sm = [c for c, _ in self.rows]
+        reasons = sorted({n for _, rs in self.rows for n in rs})
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": self.mx, "reasons": reasons, "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": self.mx, "reasons": reasons, "samples": len(sm),
+                "source": "NVML every 10 ms during the timed region"}
 
 
 # ---------------------------------------------------------------------------
@@ -342,6 +334,7 @@ def main():
     dev_ms = max_over_ranks(dev_ms)
     updates_per_step = world * tracks * K * F
     value = updates_per_step * args.steps / (dev_ms * 1e-3)
+    f.reset()
     traj = f.run_frames(dev_frames, F)
     truth = truths[0]
     rmse, mean_err, max_err = pf.accuracy_metrics(traj[0], truth)
@@ -400,6 +393,7 @@ def main():
             ms2, _ = device_steps(g, max(3, args.steps // 2))
             ms2 = max_over_ranks(ms2)
             v2 = updates_per_step * max(3, args.steps // 2) / (ms2 * 1e-3)
+            g.reset()
             t2 = g.run_frames(dev_frames, F)
             e2 = pf.accuracy_metrics(t2[0], truth)
             extra[p2] = {"value": v2, "unit": UNIT, "tracking_rmse_px": e2[0], "tracking_mean_err_px": e2[1]}

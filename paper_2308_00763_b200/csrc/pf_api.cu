@@ -166,7 +166,30 @@ struct pf_handle {
   int map_band = 32;
   bool profiling = false;
   std::vector<cudaEvent_t> pev;  // 3 per frame when profiling
+  bool use_graphs = true;
+  cudaGraphExec_t gexec = nullptr;
+  long long g_start = -1;
+  int g_cur = -1, g_F = -1;
+  const void* g_maps = nullptr;
+  const void* g_traj = nullptr;
 };
+
+typedef void (*fused_fn)(pfk::FusedArgs);
+template <int M>
+static fused_fn fused_for_vpt(int vpt) {
+  switch (vpt) {
+    case 1: return pfk::pf_fused_frame<M, 1>;
+    case 2: return pfk::pf_fused_frame<M, 2>;
+    case 4: return pfk::pf_fused_frame<M, 4>;
+    default: return pfk::pf_fused_frame<M, 8>;
+  }
+}
+static fused_fn fused_kernel(const pf_handle* h) {
+  return h->km == 0 ? fused_for_vpt<0>(h->vpt) : h->km == 1 ? fused_for_vpt<1>(h->vpt) : fused_for_vpt<2>(h->vpt);
+}
+static cudaError_t set_fused_smem(const pf_handle* h) {
+  return cudaFuncSetAttribute(fused_kernel(h), cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->fused_smem);
+}
 
 static int grow(void** p, size_t* cap, size_t bytes, std::string& err) {
   if (*cap >= bytes) return PF_OK;
@@ -201,6 +224,7 @@ int pf_destroy(pf_handle* h) {
   for (auto& e : h->ev)
     if (e) cudaEventDestroy(e);
   for (auto& e : h->pev) cudaEventDestroy(e);
+  if (h->gexec) cudaGraphExecDestroy(h->gexec);
   if (h->stream) cudaStreamDestroy(h->stream);
   delete h;
   return PF_OK;
@@ -254,7 +278,7 @@ int pf_create(pf_handle** out, const pf_config* cfg) {
   h->n_tracks = cfg->n_tracks;
   h->n_videos = cfg->n_videos;
   h->tpb = cfg->tpb ? cfg->tpb : 256;
-  h->vpt = h->tpb >= 1024 ? 1 : h->tpb >= 512 ? 2 : 4;
+  h->vpt = h->tpb >= 1024 ? 1 : h->tpb >= 512 ? 2 : h->tpb >= 256 ? 4 : 8;
   h->params = cfg->params;
   h->n_off = cfg->n_offsets;
   h->start_x = cfg->start_x;
@@ -350,7 +374,9 @@ int pf_create(pf_handle** out, const pf_config* cfg) {
   size_t rows_bytes = (size_t)(h->map_band + 2 * h->r) * h->W + 32;
   h->map_smem = 16 + 256 * h->rs + h->n_off * sizeof(int2) + h->n_plan * (sizeof(short) + sizeof(short2)) + 16 +
                 rows_bytes;
-  h->fused_smem = 3072 + PF_TILE * (h->rs + h->vs) + 232 * 8;
+  h->fused_smem = h->km == 0 ? pfk::fused_smem_bytes<0>() : h->km == 1 ? pfk::fused_smem_bytes<1>()
+                                                                      : pfk::fused_smem_bytes<2>();
+  CK(cudack(set_fused_smem(h), "fused smem attr"));
   if (h->map_smem > 48 * 1024) {
     cudaError_t ce = cudaSuccess;
     if (h->km == 0)
@@ -463,12 +489,7 @@ static int launch_frame(pf_handle* h, const void* map_slot, long long map_video_
   a.dbg_anc = h->dbg_anc;
   a.dbg_L = h->dbg_L;
   dim3 grid(h->n_tiles, h->n_tracks);
-  if (h->km == 0)
-    pfk::pf_fused_frame<0><<<grid, h->tpb, h->fused_smem, h->stream>>>(a);
-  else if (h->km == 1)
-    pfk::pf_fused_frame<1><<<grid, h->tpb, h->fused_smem, h->stream>>>(a);
-  else
-    pfk::pf_fused_frame<2><<<grid, h->tpb, h->fused_smem, h->stream>>>(a);
+  fused_kernel(h)<<<grid, h->tpb, h->fused_smem, h->stream>>>(a);
   PF_CUDA(cudaGetLastError(), h->err);
   if (h->profiling) PF_CUDA(cudaEventRecord(h->pev[3 * traj_index + 1], h->stream), h->err);
   pfk::TableArgs t{};
@@ -546,9 +567,42 @@ int pf_run(pf_handle* h, const uint8_t* frames, int32_t F, int32_t on_device, do
   if ((rc = launch_maps(h, dframes, F))) return rc;
   PF_CUDA(cudaEventRecord(h->ev[2], h->stream), h->err);
   const long long vstride = (long long)F * map_elems;  // elements between videos
-  for (int f = 0; f < F; ++f) {
-    const char* slot = (const char*)h->d_maps + (size_t)f * map_elems * h->rs;
-    if ((rc = launch_frame(h, slot, vstride, f, F))) return rc;
+  const bool graph_ok = h->use_graphs && !h->profiling && F >= 4;
+  if (graph_ok && h->gexec && h->g_start == h->frame_counter && h->g_cur == h->cur && h->g_F == F &&
+      h->g_maps == h->d_maps && h->g_traj == h->d_traj) {
+    PF_CUDA(cudaGraphLaunch(h->gexec, h->stream), h->err);
+    h->frame_counter += F;
+    if (F % 2) h->cur = 1 - h->cur;
+    h->launches += 2LL * F;
+  } else if (graph_ok) {
+    const long long start = h->frame_counter;
+    const int cur0 = h->cur;
+    cudaGraph_t g = nullptr;
+    PF_CUDA(cudaStreamBeginCapture(h->stream, cudaStreamCaptureModeThreadLocal), h->err);
+    for (int f = 0; f < F; ++f) {
+      const char* slot = (const char*)h->d_maps + (size_t)f * map_elems * h->rs;
+      if ((rc = launch_frame(h, slot, vstride, f, F))) {
+        cudaStreamEndCapture(h->stream, &g);
+        if (g) cudaGraphDestroy(g);
+        return rc;
+      }
+    }
+    PF_CUDA(cudaStreamEndCapture(h->stream, &g), h->err);
+    if (h->gexec) cudaGraphExecDestroy(h->gexec);
+    h->gexec = nullptr;
+    PF_CUDA(cudaGraphInstantiate(&h->gexec, g, 0), h->err);
+    cudaGraphDestroy(g);
+    h->g_start = start;
+    h->g_cur = cur0;
+    h->g_F = F;
+    h->g_maps = h->d_maps;
+    h->g_traj = h->d_traj;
+    PF_CUDA(cudaGraphLaunch(h->gexec, h->stream), h->err);
+  } else {
+    for (int f = 0; f < F; ++f) {
+      const char* slot = (const char*)h->d_maps + (size_t)f * map_elems * h->rs;
+      if ((rc = launch_frame(h, slot, vstride, f, F))) return rc;
+    }
   }
   PF_CUDA(cudaEventRecord(h->ev[3], h->stream), h->err);
   PF_CUDA(cudaMemcpyAsync(traj_out, h->d_traj, (size_t)h->n_tracks * F * 2 * 8, cudaMemcpyDeviceToHost, h->stream),
@@ -624,6 +678,7 @@ int pf_get_debug(pf_handle* h, int32_t track, int64_t* anc, void* loglik) {
     // enable debug capture for subsequent frames
     PF_CUDA(cudaMalloc(&h->dbg_anc, KT * 8), h->err);
     PF_CUDA(cudaMalloc(&h->dbg_L, KT * h->rs), h->err);
+    h->g_F = -1;  // captured graphs do not write the debug buffers
     return PF_OK;
   }
   PF_CUDA(cudaStreamSynchronize(h->stream), h->err);

@@ -173,7 +173,6 @@ __global__ void pf_map_wide(MapArgs a) {
   real* out = reinterpret_cast<real*>(a.maps) + (size_t)vf * a.Hm * a.Wm;
   const real denom = (real)a.denom;
   real t[128];
-  const int n = a.n_off;
   for (int e = threadIdx.x; e < (my1 - my0) * a.Wm; e += blockDim.x) {
     const int my = my0 + e / a.Wm, mx = e % a.Wm;
     const int iy = my - a.r, ix = mx - a.r;
@@ -442,129 +441,335 @@ __device__ __forceinline__ int weight_q<M_FP16>(__half L, __half m, const unsign
   return __float2int_rn(__fmul_rn(__half2float(w), 1048576.0f));  // 2^20
 }
 
+// search keys: c_j >= q  <=>  key(c_j) >= key_up(q) for non-negative values,
+// where key is the IEEE bit pattern (monotone for c >= 0) and key_up(q) the
+// bits of the smallest mode value >= q.  Exact, and integer compares only.
 template <int MODE>
-__global__ void __launch_bounds__(1024) pf_fused_frame(FusedArgs a) {
+struct Key;
+template <>
+struct Key<M_FP64> {
+  using k_t = double;
+  __device__ static __forceinline__ double of(double c) { return c; }
+  __device__ static __forceinline__ double up(double q) { return q; }
+};
+template <>
+struct Key<M_FP32> {
+  using k_t = unsigned int;
+  __device__ static __forceinline__ unsigned of(float c) { return __float_as_uint(c); }
+  __device__ static __forceinline__ unsigned up(double q) { return __float_as_uint(__double2float_ru(q)); }
+};
+template <>
+struct Key<M_FP16> {
+  using k_t = unsigned short;
+  __device__ static __forceinline__ unsigned short of(__half c) { return __half_as_ushort(c); }
+  __device__ static __forceinline__ unsigned short up(double q) {
+    __half h = __double2half(q);
+    unsigned short b = __half_as_ushort(h);
+    if ((double)__half2float(h) < q) b += 1;  // q in [0, 1]: next binary16 up
+    return b;
+  }
+};
+
+// first j in [lo, hi) with key(c[j]) >= kq (hi if none)
+template <int MODE>
+__device__ __forceinline__ int lb_key(const typename Tr<MODE>::real* c, int lo, int hi, typename Key<MODE>::k_t kq) {
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    if (Key<MODE>::of(c[mid]) < kq)
+      lo = mid + 1;
+    else
+      hi = mid;
+  }
+  return lo;
+}
+// same, knowing key(c[j0 - 1]) < kq: exponential probe from j0, then bisection
+template <int MODE>
+__device__ __forceinline__ int gallop_key(const typename Tr<MODE>::real* c, int j0, int n,
+                                          typename Key<MODE>::k_t kq) {
+  if (j0 >= n || Key<MODE>::of(c[j0]) >= kq) return j0;
+  int lo = j0 + 1, step = 1, hi = j0 + 1;
+  while (hi < n && Key<MODE>::of(c[hi]) < kq) {
+    lo = hi + 1;
+    hi += step;
+    step <<= 1;
+  }
+  if (hi > n) hi = n;
+  return lb_key<MODE>(c, lo, hi, kq);
+}
+
+template <int MODE>
+__device__ __forceinline__ bool gt_real(typename Tr<MODE>::real a, typename Tr<MODE>::real b) {
+  if constexpr (MODE == M_FP16)
+    return __hgt(a, b);
+  else
+    return a > b;
+}
+
+template <int MODE>
+__device__ __forceinline__ typename Tr<MODE>::vec to_vec(double n0, double n1) {
+  typename Tr<MODE>::vec v;
+  if constexpr (MODE == M_FP16) {
+    v = __halves2half2(__double2half(n0), __double2half(n1));
+  } else if constexpr (MODE == M_FP32) {
+    v.x = __double2float_rn(n0);
+    v.y = __double2float_rn(n1);
+  } else {
+    v.x = n0;
+    v.y = n1;
+  }
+  return v;
+}
+
+// propagate with the noise already in the mode dtype (reference arithmetic)
+template <int MODE>
+__device__ __forceinline__ typename Tr<MODE>::vec prop(typename Tr<MODE>::vec xa, typename Tr<MODE>::vec nn,
+                                                       typename Tr<MODE>::vec drift, typename Tr<MODE>::vec stdv) {
+  typename Tr<MODE>::vec o;
+  if constexpr (MODE == M_FP16) {
+    o = __hadd2_rn(__hadd2_rn(xa, drift), __hmul2_rn(stdv, nn));
+  } else if constexpr (MODE == M_FP32) {
+    o.x = __fadd_rn(__fadd_rn(xa.x, drift.x), __fmul_rn(stdv.x, nn.x));
+    o.y = __fadd_rn(__fadd_rn(xa.y, drift.y), __fmul_rn(stdv.y, nn.y));
+  } else {
+    o.x = __dadd_rn(__dadd_rn(xa.x, drift.x), __dmul_rn(stdv.x, nn.x));
+    o.y = __dadd_rn(__dadd_rn(xa.y, drift.y), __dmul_rn(stdv.y, nn.y));
+  }
+  return o;
+}
+
+template <int MODE>
+constexpr int max_src_tiles() {
+  return MODE == M_FP64 ? 3 : (MODE == M_FP32 ? 6 : 12);
+}
+
+template <int MODE>
+constexpr size_t fused_smem_bytes() {
+  using real = typename Tr<MODE>::real;
+  using vec = typename Tr<MODE>::vec;
+  return 3072 + PF_TILE * (sizeof(real) + sizeof(vec)) + max_src_tiles<MODE>() * PF_TILE * sizeof(real) +
+         (max_src_tiles<MODE>() + 1) * 24 + 256 * 8;
+}
+
+template <int MODE, int VPT>
+__global__ void __launch_bounds__(PF_TILE / VPT) pf_fused_frame(FusedArgs a) {
   using real = typename Tr<MODE>::real;
   using vec = typename Tr<MODE>::vec;
   using wq_t = typename Tr<MODE>::wq_t;
-  constexpr int VPTMAX = 4;
+  using KT = Key<MODE>;
+  constexpr int MS = max_src_tiles<MODE>();
   extern __shared__ __align__(16) unsigned char smem[];
-  uint32_t* s_kihi = reinterpret_cast<uint32_t*>(smem);            // 1 KB
-  double* s_wi = reinterpret_cast<double*>(smem + 1024);           // 2 KB
-  real* s_L = reinterpret_cast<real*>(smem + 3072);                // TILE reals
+  uint32_t* s_kihi = reinterpret_cast<uint32_t*>(smem);   // 1 KB
+  double* s_wi = reinterpret_cast<double*>(smem + 1024);  // 2 KB
+  real* s_L = reinterpret_cast<real*>(smem + 3072);
   vec* s_X = reinterpret_cast<vec*>(smem + 3072 + PF_TILE * sizeof(real));
-  unsigned char* s_misc = smem + 3072 + PF_TILE * (sizeof(real) + sizeof(vec));
-  long long* s_red = reinterpret_cast<long long*>(s_misc);         // 64 slots (scan / int moments)
-  double* s_redd = reinterpret_cast<double*>(s_misc + 64 * 8);     // 32 slots (max)
-  double* s_wx = reinterpret_cast<double*>(s_misc + 96 * 8);       // 32 slots
-  double* s_wy = reinterpret_cast<double*>(s_misc + 128 * 8);      // 32 slots
-  double* s_round = reinterpret_cast<double*>(s_misc + 160 * 8);   // 2 x 32 round values
+  real* s_c = reinterpret_cast<real*>(smem + 3072 + PF_TILE * (sizeof(real) + sizeof(vec)));
+  unsigned char* p_tab = reinterpret_cast<unsigned char*>(s_c + MS * PF_TILE);
+  long long* s_ts = reinterpret_cast<long long*>(p_tab);           // MS + 1
+  double* s_tO = reinterpret_cast<double*>(p_tab + (MS + 1) * 8);   // MS + 1
+  double* s_tM = reinterpret_cast<double*>(p_tab + (MS + 1) * 16);  // MS + 1
+  unsigned char* s_misc = p_tab + (MS + 1) * 24;
+  long long* s_red = reinterpret_cast<long long*>(s_misc);        // 64 slots
+  double* s_redd = reinterpret_cast<double*>(s_misc + 64 * 8);    // 32
+  double* s_wx = reinterpret_cast<double*>(s_misc + 96 * 8);      // 32
+  double* s_wy = reinterpret_cast<double*>(s_misc + 128 * 8);     // 32
+  double* s_round = reinterpret_cast<double*>(s_misc + 160 * 8);  // 64
   unsigned long long* s_state = reinterpret_cast<unsigned long long*>(s_misc + 224 * 8);
-  double* s_mtile = reinterpret_cast<double*>(s_misc + 225 * 8);
+  int* s_int = reinterpret_cast<int*>(s_misc + 225 * 8);          // b_lo, b_hi, staged
+  real* s_m = reinterpret_cast<real*>(s_misc + 227 * 8);
 
   const int TPB = blockDim.x;
-  const int VPT = TPB >= 1024 ? 1 : (TPB >= 512 ? 2 : VPTMAX);
   const int R = PF_TILE / (TPB * VPT);
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, nw = TPB >> 5;
   const int tile = blockIdx.x, track = blockIdx.y;
   const long long K = a.K;
   const long long base = (long long)tile * PF_TILE;
   const int Tb = (int)min((long long)PF_TILE, K - base);
-
-  for (int i = tid; i < 256; i += TPB) {
-    s_kihi[i] = (uint32_t)(PF_ZIG_KI[i] >> 20);
-    s_wi[i] = __longlong_as_double((long long)PF_ZIG_WI_BITS[i]);
-  }
-  if (tid == 0) {
-    unsigned long long pos = (unsigned long long)a.t * (unsigned long long)(2 * K + 1) + 2ULL * (unsigned long long)base;
-    s_state[0] = pfr::word_at(a.x0[track], pos);
-  }
-  __syncthreads();
-  const unsigned long long tstate = s_state[0];
+  const int n = a.n_tiles;
 
   const vec* Xp = reinterpret_cast<const vec*>(a.X_prev) + (size_t)track * K;
   vec* Xn = reinterpret_cast<vec*>(a.X_new) + (size_t)track * K;
   const real* Cp = reinterpret_cast<const real*>(a.C_prev) + (size_t)track * K;
   real* Cn = reinterpret_cast<real*>(a.C_new) + (size_t)track * K;
   const real* map = reinterpret_cast<const real*>(a.map) + (size_t)(track % a.n_videos) * a.map_video_stride;
-  const long long* ts = a.tab_s + (size_t)track * a.n_tiles;
-  const double* tO = a.tab_O + (size_t)track * a.n_tiles;
-  const double* tM = a.tab_invM + (size_t)track * a.n_tiles;
+  const long long* ts = a.tab_s + (size_t)track * n;
+  const double* tO = a.tab_O + (size_t)track * n;
+  const double* tM = a.tab_invM + (size_t)track * n;
   const double u = a.t > 0 ? a.u_prev[track] : 0.0;
   const double invK = __ddiv_rn(1.0, __ll2double_rn(K));
-  const int n = a.n_tiles;
+
+  for (int i = tid; i < 256; i += TPB) {
+    s_kihi[i] = (uint32_t)(PF_ZIG_KI[i] >> 20);
+    s_wi[i] = __longlong_as_double((long long)PF_ZIG_WI_BITS[i]);
+  }
+  if (tid == 0) {
+    const unsigned long long pos =
+        (unsigned long long)a.t * (unsigned long long)(2 * K + 1) + 2ULL * (unsigned long long)base;
+    s_state[0] = pfr::word_at(a.x0[track], pos);
+  }
+  // ---- source window of this tile's outputs (previous frame's table) ----
+  if (a.t > 0 && wid == 0) {
+    const long long kf = base, kl = base + Tb - 1;
+    const int w0 = max(0, min(tile - 16, n - 32));
+    const int bw = min(w0 + lane, n - 1);
+    const long long sv = __ldg(ts + bw);
+    int res[2];
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      const long long kk = e == 0 ? kf : kl;
+      const unsigned ball = __ballot_sync(0xffffffffu, sv <= kk);
+      const int topb = min(w0 + 31, n - 1);
+      int b = -1;
+      if (ball != 0 && (ball != 0xffffffffu || topb == n - 1)) b = min(w0 + 31 - __clz(ball), n - 1);
+      if (ball == 0xffffffffu && topb < n - 1) b = -1;
+      if (b < 0) {  // outside the window: bisection (last b with s_b <= kk)
+        int lo = 0, hi = n - 1;
+        while (lo < hi) {
+          const int mid = (lo + hi + 1) >> 1;
+          if (__ldg(ts + mid) <= kk)
+            lo = mid;
+          else
+            hi = mid - 1;
+        }
+        b = lo;
+      }
+      res[e] = b;
+    }
+    const int nsrc = res[1] - res[0] + 1;
+    const int staged = nsrc <= MS ? 1 : 0;
+    if (lane == 0) {
+      s_int[0] = res[0];
+      s_int[1] = res[1];
+      s_int[2] = staged;
+    }
+    if (staged && lane <= nsrc) {
+      const int b = min(res[0] + lane, n - 1);
+      s_ts[lane] = lane < nsrc ? __ldg(ts + b) : K;  // sentinel: s_{b_hi+1} > every k here
+      s_tO[lane] = __ldg(tO + b);
+      s_tM[lane] = __ldg(tM + b);
+    }
+  }
+  __syncthreads();
+  const unsigned long long tstate = s_state[0];
+  int b_lo = 0, b_hi = 0, staged = 0;
+  if (a.t > 0) {
+    b_lo = s_int[0];
+    b_hi = s_int[1];
+    staged = s_int[2];
+    if (staged) {
+      const long long c0 = (long long)b_lo * PF_TILE;
+      const int cnt = (int)(min((long long)(b_hi + 1) * PF_TILE, K) - c0);
+      for (int i = tid; i < cnt; i += TPB) s_c[i] = Cp[c0 + i];
+      __syncthreads();
+    }
+  }
+  const long long* Ts = staged ? s_ts - b_lo : ts;
+  const double* TO = staged ? s_tO - b_lo : tO;
+  const double* TM = staged ? s_tM - b_lo : tM;
+  const real* Csrc = staged ? s_c - (long long)b_lo * PF_TILE : Cp;
+
+  vec drift, stdv;
+  if constexpr (MODE == M_FP16) {
+    drift = __halves2half2(__double2half(a.drift_x), __double2half(a.drift_y));
+    stdv = __halves2half2(__double2half(a.std_x), __double2half(a.std_y));
+  } else {
+    drift.x = (real)a.drift_x;
+    drift.y = (real)a.drift_y;
+    stdv.x = (real)a.std_x;
+    stdv.y = (real)a.std_y;
+  }
 
   // ---------------- phase 1: resample + propagate + likelihood ----------
   real tmax = neg_inf<MODE>();
   for (int rr = 0; rr < R; ++rr) {
-    const int v = rr * TPB + tid;  // virtual thread
-    const int l0 = v * VPT;        // local index of first particle
+    const int v = rr * TPB + tid;
+    const int l0 = v * VPT;
     const long long k0 = base + l0;
-    unsigned long long xs = pfr::apply(pfr::Affine{a.tj[v].x, a.tj[v].y}, tstate);
-    long long anc[VPTMAX];
-    if (a.t == 0) {
+    long long anc[VPT];
+    if (a.t == 0 || l0 >= Tb) {
 #pragma unroll
-      for (int i = 0; i < VPTMAX; ++i) anc[i] = k0 + i;
-    } else if (l0 < Tb) {
-      // source tile of the first particle: last b with s_b <= k0
-      int lo = 0, hi = n - 1;
-      while (lo < hi) {
-        int mid = (lo + hi + 1) >> 1;
-        if (__ldg(ts + mid) <= k0)
-          lo = mid;
-        else
-          hi = mid - 1;
+      for (int i = 0; i < VPT; ++i) anc[i] = k0 + i;
+    } else {
+      // source tile of the first particle
+      int b = b_lo;
+      if (!staged) {
+        int lo = b_lo, hi = b_hi;
+        while (lo < hi) {
+          const int mid = (lo + hi + 1) >> 1;
+          if (__ldg(ts + mid) <= k0)
+            lo = mid;
+          else
+            hi = mid - 1;
+        }
+        b = lo;
       }
-      int b = lo;
       int jprev = 0, bprev = -1;
 #pragma unroll
-      for (int i = 0; i < VPTMAX; ++i) {
-        if (i >= VPT) break;
+      for (int i = 0; i < VPT; ++i) {
         const long long k = k0 + i;
         if (k >= K) {
           anc[i] = 0;
           continue;
         }
-        while (b + 1 < n && __ldg(ts + b + 1) <= k) ++b;
+        while (b < b_hi && Ts[b + 1] <= k) ++b;
         const double p = point_of<MODE>(k, u, K, invK);
-        const double im = __ldg(tM + b);
-        double q = im == 0.0 ? 0.0 : __dmul_rn(__dsub_rn(p, __ldg(tO + b)), im);
+        const double im = TM[b];
+        double q = im == 0.0 ? 0.0 : __dmul_rn(__dsub_rn(p, TO[b]), im);
         q = fmin(fmax(q, 0.0), 1.0);
+        const typename KT::k_t kq = KT::up(q);
         const long long tl = (long long)b * PF_TILE;
         const int tb = (int)min((long long)PF_TILE, K - tl);
-        const int start = (b == bprev) ? jprev : 0;
-        int j = lower_bound_c<real>(Cp + tl, start, tb, q);
+        const real* cb = Csrc + tl;
+        int j = (b == bprev) ? gallop_key<MODE>(cb, jprev, tb, kq) : lb_key<MODE>(cb, 0, tb, kq);
         j = min(j, tb - 1);
         jprev = j;
         bprev = b;
         anc[i] = tl + j;
       }
     }
+    // draws: 2 words per particle, fast ziggurat path; slow path deferred
+    unsigned long long xs = pfr::apply(pfr::Affine{a.tj[v].x, a.tj[v].y}, tstate);
+    double nr[2 * VPT];
+    unsigned long long wd[2 * VPT];
+    unsigned pend = 0;
 #pragma unroll
-    for (int i = 0; i < VPTMAX; ++i) {
-      if (i >= VPT) break;
+    for (int i = 0; i < 2 * VPT; ++i) {
+      const unsigned long long w = xs;
+      xs = pfr::kA * xs + pfr::kC;
+      wd[i] = w;
+      const unsigned idx = (unsigned)(w >> 56);
+      const unsigned long long rabs = (w >> 3) & pfr::kMask52;
+      const double x = __dmul_rn((double)rabs, s_wi[idx]);
+      nr[i] = ((w >> 55) & 1) ? -x : x;
+      if ((unsigned)(rabs >> 20) >= s_kihi[idx] && l0 + (i >> 1) < Tb) pend |= 1u << i;
+    }
+    while (__any_sync(0xffffffffu, pend != 0)) {  // one divergent pass per pending level
+      if (pend) {
+        const int i = __ffs(pend) - 1;
+        pend &= pend - 1;
+        unsigned long long wsel = 0;
+#pragma unroll
+        for (int jj = 0; jj < 2 * VPT; ++jj)
+          if (jj == i) wsel = wd[jj];
+        const double r = pfr::zig_slow(wsel);
+#pragma unroll
+        for (int jj = 0; jj < 2 * VPT; ++jj)
+          if (jj == i) nr[jj] = r;
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < VPT; ++i) {
       const int l = l0 + i;
-      const long long k = base + l;
-      const unsigned long long w0 = xs;
-      xs = pfr::kA * xs + pfr::kC;
-      const unsigned long long w1 = xs;
-      xs = pfr::kA * xs + pfr::kC;
       if (l < Tb) {
-        const double n0 = pfr::normal_of(w0, s_kihi, s_wi);
-        const double n1 = pfr::normal_of(w1, s_kihi, s_wi);
-        const vec xa = Xp[anc[i]];
-        const vec xn = propagate_one<MODE>(xa, n0, n1, a);
-        Xn[k] = xn;
-        real px, py;
-        vec_xy<MODE>(xn, px, py);
-        const int ix = round_clamp<MODE>(px, -a.r, a.W - 1 + a.r);
-        const int iy = round_clamp<MODE>(py, -a.r, a.H - 1 + a.r);
+        const vec xn = prop<MODE>(Xp[anc[i]], to_vec<MODE>(nr[2 * i], nr[2 * i + 1]), drift, stdv);
+        Xn[base + l] = xn;
+        const int ix = round_clamp<MODE>(xn.x, -a.r, a.W - 1 + a.r);
+        const int iy = round_clamp<MODE>(xn.y, -a.r, a.H - 1 + a.r);
         const real L = map[(size_t)(iy + a.r) * a.Wm + (ix + a.r)];
         s_L[l] = L;
         s_X[l] = xn;
-        if (rgt<MODE>(L, tmax)) tmax = L;
-        if (a.dbg_anc) a.dbg_anc[(size_t)track * K + k] = anc[i];
-        if (a.dbg_L) reinterpret_cast<real*>(a.dbg_L)[(size_t)track * K + k] = L;
+        if (gt_real<MODE>(L, tmax)) tmax = L;
+        if (a.dbg_anc) a.dbg_anc[(size_t)track * K + base + l] = anc[i];
+        if (a.dbg_L) reinterpret_cast<real*>(a.dbg_L)[(size_t)track * K + base + l] = L;
       } else {
         s_L[l] = neg_inf<MODE>();
         vec z;
@@ -574,50 +779,45 @@ __global__ void __launch_bounds__(1024) pf_fused_frame(FusedArgs a) {
       }
     }
   }
-  // tile max (exact: the max is one particle's L)
-  {
-    double m = to_d(tmax);
+  // tile max (exact)
 #pragma unroll
-    for (int d = 16; d >= 1; d >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, d));
-    if (lane == 0) s_redd[wid] = m;
-    __syncthreads();
-    if (tid == 0) {
-      double mm = s_redd[0];
-      for (int w = 1; w < nw; ++w) mm = fmax(mm, s_redd[w]);
-      s_mtile[0] = mm;
-    }
-    __syncthreads();
+  for (int d = 16; d >= 1; d >>= 1) {
+    const real o = __shfl_xor_sync(0xffffffffu, tmax, d);
+    if (gt_real<MODE>(o, tmax)) tmax = o;
   }
-  const double mtile_d = s_mtile[0];
-  real mtile;
-  if constexpr (MODE == M_FP16)
-    mtile = __double2half(mtile_d);
-  else
-    mtile = (real)mtile_d;
+  if (lane == 0) reinterpret_cast<real*>(s_redd)[wid] = tmax;
+  __syncthreads();
+  if (tid == 0) {
+    real mm = reinterpret_cast<real*>(s_redd)[0];
+    for (int w = 1; w < nw; ++w) {
+      const real o = reinterpret_cast<real*>(s_redd)[w];
+      if (gt_real<MODE>(o, mm)) mm = o;
+    }
+    *s_m = mm;
+  }
+  __syncthreads();
+  const real mtile = *s_m;
+  const double mtile_d = to_d(mtile);
 
   // ---------------- phase 2: weights, exact scan, local cdf, moments ------
-  // cum_j is parked in the s_X slot of particle j/(sizeof(vec)/sizeof(wq_t))
-  // once that position has been consumed (rounds advance monotonically).
   wq_t carry = 0;
-  long long mx_i = 0, my_i = 0;  // fp16 moments (exact)
+  long long mx_i = 0, my_i = 0;
   for (int rr = 0; rr < R; ++rr) {
     const int v = rr * TPB + tid;
     const int l0 = v * VPT;
-    wq_t wq[VPTMAX];
+    wq_t wq[VPT];
     wq_t loc = 0;
 #pragma unroll
-    for (int i = 0; i < VPTMAX; ++i) {
-      if (i >= VPT) break;
+    for (int i = 0; i < VPT; ++i) {
       const int l = l0 + i;
       wq[i] = (l < Tb) ? weight_q<MODE>(s_L[l], mtile, a.exp16) : (wq_t)0;
       loc += wq[i];
     }
     wq_t tot;
     const wq_t excl = block_excl_scan<wq_t>(loc, reinterpret_cast<wq_t*>(s_red), &tot);
-    double px_d[VPTMAX], py_d[VPTMAX];
+    double px_d[VPT], py_d[VPT];
 #pragma unroll
-    for (int i = 0; i < VPTMAX; ++i) {
-      if (i >= VPT) break;
+    for (int i = 0; i < VPT; ++i) {
       const vec xv = s_X[l0 + i];
       if constexpr (MODE == M_FP16) {
         const int xq = __float2int_rn(__fmul_rn(__half2float(xv.x), 1024.0f));
@@ -625,32 +825,32 @@ __global__ void __launch_bounds__(1024) pf_fused_frame(FusedArgs a) {
         mx_i += (long long)wq[i] * xq;
         my_i += (long long)wq[i] * yq;
       } else {
-        const double wd = (double)wq[i];
-        px_d[i] = __dmul_rn(wd, to_d(xv.x));
-        py_d[i] = __dmul_rn(wd, to_d(xv.y));
+        const double w = (double)wq[i];
+        px_d[i] = __dmul_rn(w, to_d(xv.x));
+        py_d[i] = __dmul_rn(w, to_d(xv.y));
       }
     }
     wq_t run = carry + excl;
 #pragma unroll
-    for (int i = 0; i < VPTMAX; ++i) {
-      if (i >= VPT) break;
+    for (int i = 0; i < VPT; ++i) {
       run += wq[i];
-      wq[i] = run;  // inclusive cum
+      wq[i] = run;
     }
-    __syncthreads();  // every position of this round has been read
+    __syncthreads();  // positions of this round consumed before cum overwrites them
 #pragma unroll
-    for (int i = 0; i < VPTMAX; ++i) {
-      if (i >= VPT) break;
-      reinterpret_cast<wq_t*>(s_X)[l0 + i] = wq[i];
-    }
+    for (int i = 0; i < VPT; ++i) reinterpret_cast<wq_t*>(s_X)[l0 + i] = wq[i];
     carry += tot;
     if constexpr (MODE != M_FP16) {
-      // canonical pairwise tree: VPT-local, lane butterfly, warps, rounds
       double sx, sy;
-      if (VPT == 4) {
+      if constexpr (VPT == 8) {
+        sx = __dadd_rn(__dadd_rn(__dadd_rn(px_d[0], px_d[1]), __dadd_rn(px_d[2], px_d[3])),
+                       __dadd_rn(__dadd_rn(px_d[4], px_d[5]), __dadd_rn(px_d[6], px_d[7])));
+        sy = __dadd_rn(__dadd_rn(__dadd_rn(py_d[0], py_d[1]), __dadd_rn(py_d[2], py_d[3])),
+                       __dadd_rn(__dadd_rn(py_d[4], py_d[5]), __dadd_rn(py_d[6], py_d[7])));
+      } else if constexpr (VPT == 4) {
         sx = __dadd_rn(__dadd_rn(px_d[0], px_d[1]), __dadd_rn(px_d[2], px_d[3]));
         sy = __dadd_rn(__dadd_rn(py_d[0], py_d[1]), __dadd_rn(py_d[2], py_d[3]));
-      } else if (VPT == 2) {
+      } else if constexpr (VPT == 2) {
         sx = __dadd_rn(px_d[0], px_d[1]);
         sy = __dadd_rn(py_d[0], py_d[1]);
       } else {
@@ -667,21 +867,24 @@ __global__ void __launch_bounds__(1024) pf_fused_frame(FusedArgs a) {
         s_wy[wid] = sy;
       }
       __syncthreads();
-      if (tid == 0) {
-        for (int width = nw; width > 1; width >>= 1)
-          for (int w = 0; w < width / 2; ++w) {
-            s_wx[w] = __dadd_rn(s_wx[2 * w], s_wx[2 * w + 1]);
-            s_wy[w] = __dadd_rn(s_wy[2 * w], s_wy[2 * w + 1]);
-          }
-        s_round[rr] = s_wx[0];
-        s_round[32 + rr] = s_wy[0];
+      if (wid == 0) {  // canonical tree over warps: butterfly with zero padding
+        double wx = lane < nw ? s_wx[lane] : 0.0;
+        double wy = lane < nw ? s_wy[lane] : 0.0;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+          wx = __dadd_rn(wx, __shfl_xor_sync(0xffffffffu, wx, d));
+          wy = __dadd_rn(wy, __shfl_xor_sync(0xffffffffu, wy, d));
+        }
+        if (lane == 0) {
+          s_round[rr] = wx;
+          s_round[32 + rr] = wy;
+        }
       }
       __syncthreads();
     }
   }
   const wq_t S = carry;
   __syncthreads();
-  // local cdf c_j = d(cum_j / S), forced to 1 where cum_j == S
   if constexpr (MODE == M_FP16) {
     const float invf = __fdiv_rn(1.0f, (float)S);
     for (int l = tid; l < Tb; l += TPB) {
@@ -699,7 +902,6 @@ __global__ void __launch_bounds__(1024) pf_fused_frame(FusedArgs a) {
         Cn[base + l] = (cum == S) ? 1.0 : cd;
     }
   }
-  // tile record
   const size_t ri = (size_t)track * n + tile;
   if constexpr (MODE == M_FP16) {
 #pragma unroll
@@ -725,6 +927,7 @@ __global__ void __launch_bounds__(1024) pf_fused_frame(FusedArgs a) {
     }
   } else {
     if (tid == 0) {
+      // tree over rounds (R is a power of two)
       for (int width = R; width > 1; width >>= 1)
         for (int w = 0; w < width / 2; ++w) {
           s_round[w] = __dadd_rn(s_round[2 * w], s_round[2 * w + 1]);
