@@ -21,9 +21,11 @@ oracle (oracle/reference_port.py), which restates halfpf's `run()`
     never saturates at large K (the reference's fp16 cumsum stalls).
 
 Per-frame structure (T = TILE particles per tile, n tiles, track = one filter):
-  1. ancestors: t == 0 -> identity; else systematic point p_k (mode formula),
-     source tile b = last b with s_b <= k, q = clamp((p_k - O_b) * invM_b, 0, 1),
-     a_k = b*T + lower_bound(c_tile_b, q).
+  1. ancestors: t == 0 -> identity; else source tile b = last b with s_b <= k,
+     local coordinate q = clamp((p_k - O_b) * invM_b, 0, 1) with the mode's
+     systematic point p_k (FP64/FP32: the reference formulas), or for FP16 the
+     f32 tile-local q = ((k - s_b) + phi_b) * rho_b, phi_b = f32(s_b + u - K O_b),
+     rho_b = f32(1/(K M_b)); a_k = b*T + lower_bound(c_tile_b, q).
   2. propagate with the LCG normals of (t, k); likelihood = map lookup.
   3. tile: m_b = max L; w_q = rint(exp(L - m_b) * 2^F); cum = inclusive scan;
      S_b = sum; c_j = d(cum_j / S_b) (forced 1 where cum_j == S_b);
@@ -123,12 +125,17 @@ class FusedTrack:
         if self.t == 0:
             return np.arange(K, dtype=np.int64)
         s, O, invM = self.table
-        p = points(self.mode, K, self.u)
         k = np.arange(K, dtype=np.int64)
         b = np.searchsorted(s, k, side="right") - 1
-        q = (p - O[b]) * invM[b]
-        q = np.where(invM[b] == 0.0, 0.0, q)
-        q = np.minimum(np.maximum(q, 0.0), 1.0)
+        if self.mode == "fp16":
+            # f32 tile-local coordinate q = ((k - s_b) + phi_b) * rho_b (table holds phi, rho)
+            q = ((k - s[b]).astype(np.float32) + O[b].astype(np.float32)) * invM[b].astype(np.float32)
+            q = np.minimum(np.maximum(q, np.float32(0.0)), np.float32(1.0)).astype(np.float64)
+        else:
+            p = points(self.mode, K, self.u)
+            q = (p - O[b]) * invM[b]
+            q = np.where(invM[b] == 0.0, 0.0, q)
+            q = np.minimum(np.maximum(q, 0.0), 1.0)
         anc = np.empty(K, dtype=np.int64)
         c64 = self.c.astype(np.float64)
         for tb in np.unique(b):
@@ -228,7 +235,14 @@ class FusedTrack:
         if mode == "fp16":
             ex *= 2.0**-XQ_BITS
             ey *= 2.0**-XQ_BITS
-        self.table = (s, O, invM)
+        if mode == "fp16":
+            Kd = np.float64(K)
+            phi = ((s.astype(np.float64) + np.float64(u)) - Kd * O).astype(np.float32)
+            with np.errstate(divide="ignore"):
+                rho = np.where(mass > 0, np.float64(Sq) / (Kd * mass.astype(np.float64)), 0.0).astype(np.float32)
+            self.table = (s, phi.astype(np.float64), rho.astype(np.float64))
+        else:
+            self.table = (s, O, invM)
         return ex, ey
 
     def step(self, Lmap: np.ndarray) -> Tuple[float, float]:

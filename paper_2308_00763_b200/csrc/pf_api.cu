@@ -17,6 +17,17 @@
 #include "../../include/pf_b200.h"
 #include "pf_kernels.cuh"
 #include "pf_staged.cuh"
+// host copies of the ziggurat tables
+#undef PF_ZIG_QUAL
+#define PF_ZIG_QUAL static const
+#define PF_ZIG_KI PF_ZIG_KI_HOST
+#define PF_ZIG_WI_BITS PF_ZIG_WI_BITS_HOST
+#define PF_ZIG_FI_BITS PF_ZIG_FI_BITS_HOST
+#define PF_ZIG_TABLES_HOST_PASS
+#include "ziggurat_tables_host.inc"
+#undef PF_ZIG_KI
+#undef PF_ZIG_WI_BITS
+#undef PF_ZIG_FI_BITS
 
 
 namespace {
@@ -143,6 +154,7 @@ struct pf_handle {
   unsigned long long* x0 = nullptr;
   ulonglong2* tj = nullptr;
   unsigned short* exp16 = nullptr;
+  void* zig = nullptr;
   int2* d_offs = nullptr;
   short* d_plan = nullptr;
   short2* d_leaves = nullptr;
@@ -217,7 +229,7 @@ int pf_destroy(pf_handle* h) {
   if (!h) return PF_OK;
   cudaSetDevice(h->device);
   void* ptrs[] = {h->X[0], h->X[1], h->C[0], h->C[1], h->rec_m, h->rec_S, h->rec_X, h->rec_Y, h->tab_s, h->tab_O,
-                  h->tab_invM, h->u, h->x0, h->tj, h->exp16, h->d_offs, h->d_plan, h->d_leaves, h->d_frames,
+                  h->tab_invM, h->u, h->x0, h->tj, h->exp16, h->zig, h->d_offs, h->d_plan, h->d_leaves, h->d_frames,
                   h->d_maps, h->d_traj, h->d_degen, h->dbg_anc, h->dbg_L};
   for (void* p : ptrs)
     if (p) cudaFree(p);
@@ -353,6 +365,17 @@ int pf_create(pf_handle** out, const pf_config* cfg) {
   build_exp16(ex.data());
   CK(cudack(cudaMalloc(&h->exp16, 65536 * 2), "exp16"));
   CK(cudack(cudaMemcpy(h->exp16, ex.data(), 65536 * 2, cudaMemcpyHostToDevice), "exp16"));
+  // ziggurat fast-path tables, packed for 16-byte smem staging
+  {
+    std::vector<unsigned char> zt(3072);
+    for (int i = 0; i < 256; ++i) {
+      uint32_t khi = (uint32_t)(PF_ZIG_KI_HOST[i] >> 20);
+      std::memcpy(zt.data() + 4 * i, &khi, 4);
+      std::memcpy(zt.data() + 1024 + 8 * i, &PF_ZIG_WI_BITS_HOST[i], 8);
+    }
+    CK(cudack(cudaMalloc(&h->zig, 3072), "zig"));
+    CK(cudack(cudaMemcpy(h->zig, zt.data(), 3072, cudaMemcpyHostToDevice), "zig"));
+  }
   // template + pairwise plan
   std::vector<int2> offs(h->n_off);
   for (int i = 0; i < h->n_off; ++i) offs[i] = make_int2(cfg->offsets_xy[2 * i], cfg->offsets_xy[2 * i + 1]);
@@ -488,6 +511,7 @@ static int launch_frame(pf_handle* h, const void* map_slot, long long map_video_
   a.std_y = h->params.std_y;
   a.dbg_anc = h->dbg_anc;
   a.dbg_L = h->dbg_L;
+  a.zig = h->zig;
   dim3 grid(h->n_tiles, h->n_tracks);
   fused_kernel(h)<<<grid, h->tpb, h->fused_smem, h->stream>>>(a);
   PF_CUDA(cudaGetLastError(), h->err);
@@ -511,7 +535,7 @@ static int launch_frame(pf_handle* h, const void* map_slot, long long map_video_
   t.traj_stride = traj_stride;
   t.traj_index = traj_index;
   t.degenerate = h->d_degen;
-  const size_t tsm = 32 * 8 + 100 * 8;
+  const size_t tsm = 0;
   if (h->km == 0)
     pfk::pf_tile_table<0><<<h->n_tracks, h->tpb_table, tsm, h->stream>>>(t);
   else if (h->km == 1)

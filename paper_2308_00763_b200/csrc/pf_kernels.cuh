@@ -301,6 +301,7 @@ struct FusedArgs {
   double drift_x, drift_y, std_x, std_y;
   long long* dbg_anc;  // optional
   void* dbg_L;         // optional
+  const void* zig;     // packed ziggurat fast-path tables: ki>>20 (u32 x 256) then wi (f64 x 256)
 };
 
 template <typename T>
@@ -542,12 +543,52 @@ constexpr int max_src_tiles() {
   return MODE == M_FP64 ? 3 : (MODE == M_FP32 ? 6 : 12);
 }
 
+constexpr int kSlowQ = 256;  // deferred ziggurat slow paths per CTA (overflow -> inline)
+
 template <int MODE>
 constexpr size_t fused_smem_bytes() {
   using real = typename Tr<MODE>::real;
   using vec = typename Tr<MODE>::vec;
-  return 3072 + PF_TILE * (sizeof(real) + sizeof(vec)) + max_src_tiles<MODE>() * PF_TILE * sizeof(real) +
-         (max_src_tiles<MODE>() + 1) * 24 + 256 * 8;
+  return 4096 + PF_TILE * (sizeof(real) + sizeof(vec)) + max_src_tiles<MODE>() * PF_TILE * sizeof(real) +
+         (max_src_tiles<MODE>() + 1) * 24 + kSlowQ * 16 + 256 * 8;
+}
+
+// branchless lower bound: first j in [0, n) with key(c[j]) >= kq, n if none
+template <int MODE>
+__device__ __forceinline__ int lb_branchless(const typename Tr<MODE>::real* c, int n, typename Key<MODE>::k_t kq) {
+  int lo = 0;  // invariant: answer in [lo, lo + len]
+  int len = n;
+  while (len > 0) {
+    const int half = len >> 1;
+    const bool lt = Key<MODE>::of(c[lo + half]) < kq;
+    lo = lt ? lo + half + 1 : lo;
+    len = lt ? len - half - 1 : half;
+  }
+  return lo;
+}
+// from a known position: short linear probe, then exponential + bisection
+template <int MODE>
+__device__ __forceinline__ int advance_key(const typename Tr<MODE>::real* c, int j0, int n,
+                                           typename Key<MODE>::k_t kq) {
+#pragma unroll
+  for (int s = 0; s < 4; ++s) {
+    if (j0 >= n || Key<MODE>::of(c[j0]) >= kq) return j0;
+    ++j0;
+  }
+  return gallop_key<MODE>(c, j0, n, kq);
+}
+
+template <int MODE>
+__device__ __forceinline__ void set_comp(typename Tr<MODE>::vec& v, int comp, double x) {
+  if constexpr (MODE == M_FP16) {
+    const __half h = __double2half(x);
+    v = comp ? __halves2half2(__low2half(v), h) : __halves2half2(h, __high2half(v));
+  } else {
+    if (comp)
+      v.y = (typename Tr<MODE>::real)x;
+    else
+      v.x = (typename Tr<MODE>::real)x;
+  }
 }
 
 template <int MODE, int VPT>
@@ -560,22 +601,24 @@ __global__ void __launch_bounds__(PF_TILE / VPT) pf_fused_frame(FusedArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
   uint32_t* s_kihi = reinterpret_cast<uint32_t*>(smem);   // 1 KB
   double* s_wi = reinterpret_cast<double*>(smem + 1024);  // 2 KB
-  real* s_L = reinterpret_cast<real*>(smem + 3072);
-  vec* s_X = reinterpret_cast<vec*>(smem + 3072 + PF_TILE * sizeof(real));
-  real* s_c = reinterpret_cast<real*>(smem + 3072 + PF_TILE * (sizeof(real) + sizeof(vec)));
+  real* s_L = reinterpret_cast<real*>(smem + 4096);
+  vec* s_X = reinterpret_cast<vec*>(smem + 4096 + PF_TILE * sizeof(real));  // normals, then positions, then cum
+  real* s_c = reinterpret_cast<real*>(smem + 4096 + PF_TILE * (sizeof(real) + sizeof(vec)));
   unsigned char* p_tab = reinterpret_cast<unsigned char*>(s_c + MS * PF_TILE);
   long long* s_ts = reinterpret_cast<long long*>(p_tab);           // MS + 1
   double* s_tO = reinterpret_cast<double*>(p_tab + (MS + 1) * 8);   // MS + 1
   double* s_tM = reinterpret_cast<double*>(p_tab + (MS + 1) * 16);  // MS + 1
-  unsigned char* s_misc = p_tab + (MS + 1) * 24;
-  long long* s_red = reinterpret_cast<long long*>(s_misc);        // 64 slots
+  unsigned long long* s_qw = reinterpret_cast<unsigned long long*>(p_tab + (MS + 1) * 24);
+  int* s_qs = reinterpret_cast<int*>(s_qw + kSlowQ);
+  unsigned char* s_misc = reinterpret_cast<unsigned char*>(s_qs + 2 * kSlowQ);
+  long long* s_red = reinterpret_cast<long long*>(s_misc);        // 64
   double* s_redd = reinterpret_cast<double*>(s_misc + 64 * 8);    // 32
   double* s_wx = reinterpret_cast<double*>(s_misc + 96 * 8);      // 32
   double* s_wy = reinterpret_cast<double*>(s_misc + 128 * 8);     // 32
   double* s_round = reinterpret_cast<double*>(s_misc + 160 * 8);  // 64
   unsigned long long* s_state = reinterpret_cast<unsigned long long*>(s_misc + 224 * 8);
-  int* s_int = reinterpret_cast<int*>(s_misc + 225 * 8);          // b_lo, b_hi, staged
-  real* s_m = reinterpret_cast<real*>(s_misc + 227 * 8);
+  int* s_int = reinterpret_cast<int*>(s_misc + 225 * 8);  // b_lo, b_hi, staged, queue count
+  real* s_m = reinterpret_cast<real*>(s_misc + 228 * 8);
 
   const int TPB = blockDim.x;
   const int R = PF_TILE / (TPB * VPT);
@@ -597,14 +640,17 @@ __global__ void __launch_bounds__(PF_TILE / VPT) pf_fused_frame(FusedArgs a) {
   const double u = a.t > 0 ? a.u_prev[track] : 0.0;
   const double invK = __ddiv_rn(1.0, __ll2double_rn(K));
 
-  for (int i = tid; i < 256; i += TPB) {
-    s_kihi[i] = (uint32_t)(PF_ZIG_KI[i] >> 20);
-    s_wi[i] = __longlong_as_double((long long)PF_ZIG_WI_BITS[i]);
+  {
+    const uint4* zsrc = reinterpret_cast<const uint4*>(a.zig);  // {ki_hi x4} / {wi x2} packed 16 B
+    uint4* zdst = reinterpret_cast<uint4*>(smem);
+    for (int i = tid; i < 192; i += TPB) zdst[i] = zsrc[i];
   }
   if (tid == 0) {
     const unsigned long long pos =
         (unsigned long long)a.t * (unsigned long long)(2 * K + 1) + 2ULL * (unsigned long long)base;
     s_state[0] = pfr::word_at(a.x0[track], pos);
+    s_int[3] = 0;  // slow-path queue counters (alternate per round)
+    s_int[4] = 0;
   }
   // ---- source window of this tile's outputs (previous frame's table) ----
   if (a.t > 0 && wid == 0) {
@@ -620,8 +666,7 @@ __global__ void __launch_bounds__(PF_TILE / VPT) pf_fused_frame(FusedArgs a) {
       const int topb = min(w0 + 31, n - 1);
       int b = -1;
       if (ball != 0 && (ball != 0xffffffffu || topb == n - 1)) b = min(w0 + 31 - __clz(ball), n - 1);
-      if (ball == 0xffffffffu && topb < n - 1) b = -1;
-      if (b < 0) {  // outside the window: bisection (last b with s_b <= kk)
+      if (b < 0) {
         int lo = 0, hi = n - 1;
         while (lo < hi) {
           const int mid = (lo + hi + 1) >> 1;
@@ -643,7 +688,7 @@ __global__ void __launch_bounds__(PF_TILE / VPT) pf_fused_frame(FusedArgs a) {
     }
     if (staged && lane <= nsrc) {
       const int b = min(res[0] + lane, n - 1);
-      s_ts[lane] = lane < nsrc ? __ldg(ts + b) : K;  // sentinel: s_{b_hi+1} > every k here
+      s_ts[lane] = lane < nsrc ? __ldg(ts + b) : K;
       s_tO[lane] = __ldg(tO + b);
       s_tM[lane] = __ldg(tM + b);
     }
@@ -655,10 +700,19 @@ __global__ void __launch_bounds__(PF_TILE / VPT) pf_fused_frame(FusedArgs a) {
     b_lo = s_int[0];
     b_hi = s_int[1];
     staged = s_int[2];
-    if (staged) {
+    if (staged) {  // 16-byte copies of the source tiles' local CDFs
       const long long c0 = (long long)b_lo * PF_TILE;
       const int cnt = (int)(min((long long)(b_hi + 1) * PF_TILE, K) - c0);
-      for (int i = tid; i < cnt; i += TPB) s_c[i] = Cp[c0 + i];
+      constexpr int PER = 16 / sizeof(real);
+      const int nvec = cnt / PER;
+      const uint4* src = reinterpret_cast<const uint4*>(Cp + c0);
+      uint4* dst = reinterpret_cast<uint4*>(s_c);
+      if ((((size_t)track * K) % PER) == 0) {
+        for (int i = tid; i < nvec; i += TPB) dst[i] = __ldg(src + i);
+        for (int i = nvec * PER + tid; i < cnt; i += TPB) s_c[i] = Cp[c0 + i];
+      } else {
+        for (int i = tid; i < cnt; i += TPB) s_c[i] = Cp[c0 + i];
+      }
       __syncthreads();
     }
   }
@@ -684,12 +738,50 @@ __global__ void __launch_bounds__(PF_TILE / VPT) pf_fused_frame(FusedArgs a) {
     const int v = rr * TPB + tid;
     const int l0 = v * VPT;
     const long long k0 = base + l0;
+    // (a) draws: fast ziggurat path into s_X (as mode-dtype noise); slow
+    //     paths queued for one CTA-wide pass
+    {
+      unsigned long long xs = pfr::apply(pfr::Affine{a.tj[v].x, a.tj[v].y}, tstate);
+#pragma unroll
+      for (int i = 0; i < VPT; ++i) {
+        double nn[2];
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+          const unsigned long long w = xs;
+          xs = pfr::kA * xs + pfr::kC;
+          const unsigned idx = (unsigned)(w >> 56);
+          const unsigned long long rabs = (w >> 3) & pfr::kMask52;
+          const double x = __dmul_rn((double)rabs, s_wi[idx]);
+          nn[c] = ((w >> 55) & 1) ? -x : x;
+          if ((unsigned)(rabs >> 20) >= s_kihi[idx] && l0 + i < Tb) {
+            const int slot = atomicAdd(&s_int[3 + (rr & 1)], 1);
+            if (slot < kSlowQ) {
+              s_qw[slot] = w;
+              s_qs[slot] = (l0 + i) * 2 + c;
+            } else {
+              nn[c] = pfr::zig_slow(w);  // queue overflow (never in practice)
+            }
+          }
+        }
+        s_X[l0 + i] = to_vec<MODE>(nn[0], nn[1]);
+      }
+    }
+    __syncthreads();
+    {
+      const int nq = min(s_int[3 + (rr & 1)], kSlowQ);
+      for (int e = tid; e < nq; e += TPB) {
+        const int sl = s_qs[e];
+        set_comp<MODE>(s_X[sl >> 1], sl & 1, pfr::zig_slow(s_qw[e]));
+      }
+    }
+    __syncthreads();
+    if (tid == 0) s_int[3 + (rr & 1)] = 0;  // reused by round rr + 2, after round rr + 1's barriers
+    // (b) ancestors
     long long anc[VPT];
     if (a.t == 0 || l0 >= Tb) {
 #pragma unroll
       for (int i = 0; i < VPT; ++i) anc[i] = k0 + i;
     } else {
-      // source tile of the first particle
       int b = b_lo;
       if (!staged) {
         int lo = b_lo, hi = b_hi;
@@ -707,64 +799,41 @@ __global__ void __launch_bounds__(PF_TILE / VPT) pf_fused_frame(FusedArgs a) {
       for (int i = 0; i < VPT; ++i) {
         const long long k = k0 + i;
         if (k >= K) {
-          anc[i] = 0;
+          anc[i] = k;
           continue;
         }
         while (b < b_hi && Ts[b + 1] <= k) ++b;
-        const double p = point_of<MODE>(k, u, K, invK);
-        const double im = TM[b];
-        double q = im == 0.0 ? 0.0 : __dmul_rn(__dsub_rn(p, TO[b]), im);
-        q = fmin(fmax(q, 0.0), 1.0);
-        const typename KT::k_t kq = KT::up(q);
+        typename KT::k_t kq;
+        if constexpr (MODE == M_FP16) {
+          // tile-local point: q = ((k - s_b) + phi_b) * rho_b in f32 (phi, rho from the table)
+          const float qf = __fmul_rn(__fadd_rn((float)(int)(k - Ts[b]), (float)TO[b]), (float)TM[b]);
+          kq = __half_as_ushort(__float2half_ru(fminf(fmaxf(qf, 0.0f), 1.0f)));
+        } else {
+          const double p = point_of<MODE>(k, u, K, invK);
+          const double im = TM[b];
+          double q = im == 0.0 ? 0.0 : __dmul_rn(__dsub_rn(p, TO[b]), im);
+          kq = KT::up(fmin(fmax(q, 0.0), 1.0));
+        }
         const long long tl = (long long)b * PF_TILE;
         const int tb = (int)min((long long)PF_TILE, K - tl);
         const real* cb = Csrc + tl;
-        int j = (b == bprev) ? gallop_key<MODE>(cb, jprev, tb, kq) : lb_key<MODE>(cb, 0, tb, kq);
+        int j = (b == bprev) ? advance_key<MODE>(cb, jprev, tb, kq) : lb_branchless<MODE>(cb, tb, kq);
         j = min(j, tb - 1);
         jprev = j;
         bprev = b;
         anc[i] = tl + j;
       }
     }
-    // draws: 2 words per particle, fast ziggurat path; slow path deferred
-    unsigned long long xs = pfr::apply(pfr::Affine{a.tj[v].x, a.tj[v].y}, tstate);
-    double nr[2 * VPT];
-    unsigned long long wd[2 * VPT];
-    unsigned pend = 0;
-#pragma unroll
-    for (int i = 0; i < 2 * VPT; ++i) {
-      const unsigned long long w = xs;
-      xs = pfr::kA * xs + pfr::kC;
-      wd[i] = w;
-      const unsigned idx = (unsigned)(w >> 56);
-      const unsigned long long rabs = (w >> 3) & pfr::kMask52;
-      const double x = __dmul_rn((double)rabs, s_wi[idx]);
-      nr[i] = ((w >> 55) & 1) ? -x : x;
-      if ((unsigned)(rabs >> 20) >= s_kihi[idx] && l0 + (i >> 1) < Tb) pend |= 1u << i;
-    }
-    while (__any_sync(0xffffffffu, pend != 0)) {  // one divergent pass per pending level
-      if (pend) {
-        const int i = __ffs(pend) - 1;
-        pend &= pend - 1;
-        unsigned long long wsel = 0;
-#pragma unroll
-        for (int jj = 0; jj < 2 * VPT; ++jj)
-          if (jj == i) wsel = wd[jj];
-        const double r = pfr::zig_slow(wsel);
-#pragma unroll
-        for (int jj = 0; jj < 2 * VPT; ++jj)
-          if (jj == i) nr[jj] = r;
-      }
-    }
+    // (c) gather + propagate + likelihood
 #pragma unroll
     for (int i = 0; i < VPT; ++i) {
       const int l = l0 + i;
       if (l < Tb) {
-        const vec xn = prop<MODE>(Xp[anc[i]], to_vec<MODE>(nr[2 * i], nr[2 * i + 1]), drift, stdv);
+        const vec xn = prop<MODE>(Xp[anc[i]], s_X[l], drift, stdv);
         Xn[base + l] = xn;
         const int ix = round_clamp<MODE>(xn.x, -a.r, a.W - 1 + a.r);
         const int iy = round_clamp<MODE>(xn.y, -a.r, a.H - 1 + a.r);
-        const real L = map[(size_t)(iy + a.r) * a.Wm + (ix + a.r)];
+        const real L = map[(iy + a.r) * a.Wm + (ix + a.r)];
         s_L[l] = L;
         s_X[l] = xn;
         if (gt_real<MODE>(L, tmax)) tmax = L;
@@ -802,6 +871,7 @@ __global__ void __launch_bounds__(PF_TILE / VPT) pf_fused_frame(FusedArgs a) {
   // ---------------- phase 2: weights, exact scan, local cdf, moments ------
   wq_t carry = 0;
   long long mx_i = 0, my_i = 0;
+  wq_t cum_r[VPT];  // R == 1: inclusive cum stays in registers
   for (int rr = 0; rr < R; ++rr) {
     const int v = rr * TPB + tid;
     const int l0 = v * VPT;
@@ -834,11 +904,13 @@ __global__ void __launch_bounds__(PF_TILE / VPT) pf_fused_frame(FusedArgs a) {
 #pragma unroll
     for (int i = 0; i < VPT; ++i) {
       run += wq[i];
-      wq[i] = run;
+      cum_r[i] = run;
     }
-    __syncthreads();  // positions of this round consumed before cum overwrites them
+    if (R > 1) {
+      __syncthreads();  // positions of this round consumed before cum overwrites them
 #pragma unroll
-    for (int i = 0; i < VPT; ++i) reinterpret_cast<wq_t*>(s_X)[l0 + i] = wq[i];
+      for (int i = 0; i < VPT; ++i) reinterpret_cast<wq_t*>(s_X)[l0 + i] = cum_r[i];
+    }
     carry += tot;
     if constexpr (MODE != M_FP16) {
       double sx, sy;
@@ -884,23 +956,49 @@ __global__ void __launch_bounds__(PF_TILE / VPT) pf_fused_frame(FusedArgs a) {
     }
   }
   const wq_t S = carry;
-  __syncthreads();
-  if constexpr (MODE == M_FP16) {
-    const float invf = __fdiv_rn(1.0f, (float)S);
-    for (int l = tid; l < Tb; l += TPB) {
-      const int cum = reinterpret_cast<const int*>(s_X)[l];
-      Cn[base + l] = (cum == S) ? __float2half(1.0f) : __float2half_rn(__fmul_rn((float)cum, invf));
-    }
-  } else {
-    const double inv = __ddiv_rn(1.0, (double)S);
-    for (int l = tid; l < Tb; l += TPB) {
-      const long long cum = reinterpret_cast<const long long*>(s_X)[l];
+  // local cdf c_j = d(cum_j / S), forced to 1 where cum_j == S
+  auto cdf_of = [&](wq_t cum) -> real {
+    if constexpr (MODE == M_FP16) {
+      const float invf = __fdiv_rn(1.0f, (float)S);
+      return (cum == S) ? __float2half(1.0f) : __float2half_rn(__fmul_rn((float)cum, invf));
+    } else {
+      const double inv = __ddiv_rn(1.0, (double)S);
       const double cd = __dmul_rn((double)cum, inv);
       if constexpr (MODE == M_FP32)
-        Cn[base + l] = (cum == S) ? 1.0f : __double2float_rn(cd);
+        return (cum == S) ? 1.0f : __double2float_rn(cd);
       else
-        Cn[base + l] = (cum == S) ? 1.0 : cd;
+        return (cum == S) ? 1.0 : cd;
     }
+  };
+  if (R == 1) {
+    const int l0 = tid * VPT;
+    real cv[VPT];
+#pragma unroll
+    for (int i = 0; i < VPT; ++i) cv[i] = cdf_of(cum_r[i]);
+    constexpr int VB = VPT * (int)sizeof(real);
+    if (l0 + VPT <= Tb && (VB == 4 || VB == 8 || VB == 16) &&
+        ((((size_t)track * K + base + l0) * sizeof(real)) % VB) == 0) {
+      if constexpr (VB == 16) {
+        uint4 o;
+        memcpy(&o, cv, 16);
+        *reinterpret_cast<uint4*>(Cn + base + l0) = o;
+      } else if constexpr (VB == 8) {
+        uint2 o;
+        memcpy(&o, cv, 8);
+        *reinterpret_cast<uint2*>(Cn + base + l0) = o;
+      } else if constexpr (VB == 4) {
+        unsigned o;
+        memcpy(&o, cv, 4);
+        *reinterpret_cast<unsigned*>(Cn + base + l0) = o;
+      }
+    } else {
+#pragma unroll
+      for (int i = 0; i < VPT; ++i)
+        if (l0 + i < Tb) Cn[base + l0 + i] = cv[i];
+    }
+  } else {
+    __syncthreads();
+    for (int l = tid; l < Tb; l += TPB) Cn[base + l] = cdf_of(reinterpret_cast<const wq_t*>(s_X)[l]);
   }
   const size_t ri = (size_t)track * n + tile;
   if constexpr (MODE == M_FP16) {
@@ -927,7 +1025,6 @@ __global__ void __launch_bounds__(PF_TILE / VPT) pf_fused_frame(FusedArgs a) {
     }
   } else {
     if (tid == 0) {
-      // tree over rounds (R is a power of two)
       for (int width = R; width > 1; width >>= 1)
         for (int w = 0; w < width / 2; ++w) {
           s_round[w] = __dadd_rn(s_round[2 * w], s_round[2 * w + 1]);
@@ -988,9 +1085,8 @@ struct PwAcc {
 
 template <int MODE>
 __global__ void __launch_bounds__(1024) pf_tile_table(TableArgs a) {
-  extern __shared__ __align__(16) unsigned char smem[];
-  long long* s_i = reinterpret_cast<long long*>(smem);     // 32
-  double* s_d = reinterpret_cast<double*>(smem + 32 * 8);  // 3 x 32 + 2
+  __shared__ long long s_i[32];
+  __shared__ double s_d[3 * 32 + 4];
   constexpr int FB = Tr<MODE>::FB;
   const int track = blockIdx.x, tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const int TPB = blockDim.x, nw = TPB >> 5;
@@ -1002,117 +1098,191 @@ __global__ void __launch_bounds__(1024) pf_tile_table(TableArgs a) {
   const long long* rX = a.rec_X + (size_t)track * n;
   const long long* rY = a.rec_Y + (size_t)track * n;
 
-  // 1. global max (exact) + the frame's resampling uniform
-  double m = __longlong_as_double(0xfff0000000000000LL);
-  for (int i = 0; i < Rt; ++i)
-    if (b0 + i < n) m = fmax(m, rm[b0 + i]);
-#pragma unroll
-  for (int d = 16; d >= 1; d >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, d));
-  if (lane == 0) s_d[wid] = m;
-  __syncthreads();
-  if (tid == 0) {
-    double mm = s_d[0];
-    for (int w = 1; w < nw; ++w) mm = fmax(mm, s_d[w]);
-    s_d[96] = mm;
+  // the frame's resampling uniform (stream position t(2K+1)+2K), computed by
+  // a warp other than warp 0 while the max reduction proceeds
+  if (tid == (nw > 1 ? 32 : 0)) {
     const unsigned long long pos =
         (unsigned long long)a.t * (unsigned long long)(2 * a.K + 1) + 2ULL * (unsigned long long)a.K;
     s_d[97] = pfr::uniform_of(pfr::word_at(a.x0[track], pos));
   }
+  // 1. global max (exact)
+  double m = __longlong_as_double(0xfff0000000000000LL);
+  double m1 = m;
+  long long S1 = 0, X1 = 0, Y1 = 0;
+  if (Rt == 1 && b0 < n) {  // common case: one tile per thread, keep it in registers
+    m1 = rm[b0];
+    S1 = rS[b0];
+    X1 = rX[b0];
+    Y1 = rY[b0];
+    m = m1;
+  } else {
+    for (int i = 0; i < Rt; ++i)
+      if (b0 + i < n) m = fmax(m, rm[b0 + i]);
+  }
+#pragma unroll
+  for (int d = 16; d >= 1; d >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, d));
+  if (lane == 0) s_d[wid] = m;
+  __syncthreads();
+  if (wid == 0) {
+    double mm = lane < nw ? s_d[lane] : s_d[0];
+#pragma unroll
+    for (int d = 16; d >= 1; d >>= 1) mm = fmax(mm, __shfl_xor_sync(0xffffffffu, mm, d));
+    if (lane == 0) s_d[96] = mm;
+  }
   __syncthreads();
   m = s_d[96];
   const double u = s_d[97];
-  __syncthreads();
   const double scale = ldexp(1.0, a.Q - FB);
+  const double Kd = __ll2double_rn(a.K);
+  const double invK = __ddiv_rn(1.0, Kd);
 
-  // 2. exact fixed-point tile masses and their prefix
-  long long loc = 0;
-  for (int i = 0; i < Rt; ++i) {
-    const int b = b0 + i;
-    if (b < n) {
-      const double f = pfm::exp64(__dsub_rn(rm[b], m));
-      loc += __double2ll_rn(__dmul_rn(__dmul_rn((double)rS[b], f), scale));
+  auto tile_mass = [&](double mb, long long Sb, double& f) -> long long {
+    f = pfm::exp64(__dsub_rn(mb, m));
+    return __double2ll_rn(__dmul_rn(__dmul_rn((double)Sb, f), scale));
+  };
+  // first output index of tile b: #points <= O (exact for the mode's point formula)
+  auto first_output = [&](double O) -> long long {
+    long long k = (long long)floor(__dsub_rn(__dmul_rn(O, Kd), u));
+    k = min(max(k, 0LL), a.K);
+    while (k > 0 && point_of<MODE>(k - 1, u, a.K, invK) > O) --k;
+    while (k < a.K && point_of<MODE>(k, u, a.K, invK) <= O) ++k;
+    return k;
+  };
+
+  // resampling geometry of tile b.  FP64/FP32: offset O_b and 1/M_b (the
+  // reference's point formula is evaluated against them).  FP16: the f32
+  // tile-local coordinate q = ((k - s_b) + phi_b) * rho_b with
+  // phi_b = f32(s_b + u - K O_b), rho_b = f32(1 / (K M_b)).
+  auto store_tile_geometry = [&](size_t ti, long long sb, double O, long long mass, double Sq) {
+    if constexpr (MODE == M_FP16) {
+      a.tab_O[ti] = (double)__double2float_rn(__dsub_rn(__dadd_rn((double)sb, u), __dmul_rn(Kd, O)));
+      a.tab_invM[ti] = mass > 0 ? (double)__double2float_rn(__ddiv_rn(Sq, __dmul_rn(Kd, (double)mass))) : 0.0;
+    } else {
+      a.tab_O[ti] = O;
+      a.tab_invM[ti] = mass > 0 ? __ddiv_rn(Sq, (double)mass) : 0.0;
     }
-  }
-  long long tot;
-  const long long excl = block_excl_scan<long long>(loc, s_i, &tot);
-  const double Sq = (double)tot;
-  const double invK = __ddiv_rn(1.0, __ll2double_rn(a.K));
+  };
 
-  // 3. table entries + estimate moments (canonical tree over padded tiles)
-  long long run = excl;
-  PwAcc ax, ay, ad;
-  ax.reset();
-  ay.reset();
-  ad.reset();
-  for (int i = 0; i < Rt; ++i) {
-    const int b = b0 + i;
+  if (Rt == 1) {
+    const int b = b0;
+    double f = 0.0;
+    const long long mass = b < n ? tile_mass(m1, S1, f) : 0;
+    long long tot;
+    const long long excl = block_excl_scan<long long>(mass, s_i, &tot);
+    const double Sq = (double)tot;
     double vx = 0.0, vy = 0.0, vd = 0.0;
     if (b < n) {
-      const double f = pfm::exp64(__dsub_rn(rm[b], m));
-      const long long mass = __double2ll_rn(__dmul_rn(__dmul_rn((double)rS[b], f), scale));
-      const double O = __ddiv_rn((double)run, Sq);
-      const double invM = mass > 0 ? __ddiv_rn(Sq, (double)mass) : 0.0;
-      long long s = 0;
-      if (b > 0) {
-        long long k = (long long)floor(__dsub_rn(__dmul_rn(O, (double)a.K), u));
-        k = min(max(k, 0LL), a.K);
-        while (k > 0 && point_of<MODE>(k - 1, u, a.K, invK) > O) --k;
-        while (k < a.K && point_of<MODE>(k, u, a.K, invK) <= O) ++k;
-        s = k;
-      }
+      const double O = __ddiv_rn((double)excl, Sq);
       const size_t ti = (size_t)track * n + b;
-      a.tab_s[ti] = s;
-      a.tab_O[ti] = O;
-      a.tab_invM[ti] = invM;
+      const long long sb = b > 0 ? first_output(O) : 0;
+      a.tab_s[ti] = sb;
+      store_tile_geometry(ti, sb, O, mass, Sq);
       double X, Y;
       if constexpr (MODE == M_FP16) {
-        X = (double)rX[b];
-        Y = (double)rY[b];
+        X = (double)X1;
+        Y = (double)Y1;
       } else {
-        X = __longlong_as_double(rX[b]);
-        Y = __longlong_as_double(rY[b]);
+        X = __longlong_as_double(X1);
+        Y = __longlong_as_double(Y1);
       }
       vx = __dmul_rn(f, X);
       vy = __dmul_rn(f, Y);
-      vd = __dmul_rn(f, (double)rS[b]);
-      run += mass;
+      vd = __dmul_rn(f, (double)S1);
     }
-    ax.push(vx);
-    ay.push(vy);
-    ad.push(vd);
-  }
-  double nx = ax.root(), ny = ay.root(), den = ad.root();
+    // canonical pairwise tree: lanes then warps (butterflies, zero padding)
 #pragma unroll
-  for (int d = 1; d < 32; d <<= 1) {
-    nx = __dadd_rn(nx, __shfl_xor_sync(0xffffffffu, nx, d));
-    ny = __dadd_rn(ny, __shfl_xor_sync(0xffffffffu, ny, d));
-    den = __dadd_rn(den, __shfl_xor_sync(0xffffffffu, den, d));
-  }
-  if (lane == 0) {
-    s_d[wid] = nx;
-    s_d[32 + wid] = ny;
-    s_d[64 + wid] = den;
+    for (int d = 1; d < 32; d <<= 1) {
+      vx = __dadd_rn(vx, __shfl_xor_sync(0xffffffffu, vx, d));
+      vy = __dadd_rn(vy, __shfl_xor_sync(0xffffffffu, vy, d));
+      vd = __dadd_rn(vd, __shfl_xor_sync(0xffffffffu, vd, d));
+    }
+    if (lane == 0) {
+      s_d[wid] = vx;
+      s_d[32 + wid] = vy;
+      s_d[64 + wid] = vd;
+    }
+  } else {
+    long long loc = 0;
+    for (int i = 0; i < Rt; ++i) {
+      const int b = b0 + i;
+      if (b < n) {
+        double f;
+        loc += tile_mass(rm[b], rS[b], f);
+      }
+    }
+    long long tot;
+    const long long excl = block_excl_scan<long long>(loc, s_i, &tot);
+    const double Sq = (double)tot;
+    long long run = excl;
+    PwAcc ax, ay, ad;
+    ax.reset();
+    ay.reset();
+    ad.reset();
+    for (int i = 0; i < Rt; ++i) {
+      const int b = b0 + i;
+      double vx = 0.0, vy = 0.0, vd = 0.0;
+      if (b < n) {
+        double f;
+        const long long mass = tile_mass(rm[b], rS[b], f);
+        const double O = __ddiv_rn((double)run, Sq);
+        const size_t ti = (size_t)track * n + b;
+        const long long sb = b > 0 ? first_output(O) : 0;
+        a.tab_s[ti] = sb;
+        store_tile_geometry(ti, sb, O, mass, Sq);
+        double X, Y;
+        if constexpr (MODE == M_FP16) {
+          X = (double)rX[b];
+          Y = (double)rY[b];
+        } else {
+          X = __longlong_as_double(rX[b]);
+          Y = __longlong_as_double(rY[b]);
+        }
+        vx = __dmul_rn(f, X);
+        vy = __dmul_rn(f, Y);
+        vd = __dmul_rn(f, (double)rS[b]);
+        run += mass;
+      }
+      ax.push(vx);
+      ay.push(vy);
+      ad.push(vd);
+    }
+    double nx = ax.root(), ny = ay.root(), den = ad.root();
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      nx = __dadd_rn(nx, __shfl_xor_sync(0xffffffffu, nx, d));
+      ny = __dadd_rn(ny, __shfl_xor_sync(0xffffffffu, ny, d));
+      den = __dadd_rn(den, __shfl_xor_sync(0xffffffffu, den, d));
+    }
+    if (lane == 0) {
+      s_d[wid] = nx;
+      s_d[32 + wid] = ny;
+      s_d[64 + wid] = den;
+    }
   }
   __syncthreads();
-  if (tid == 0) {
-    for (int width = nw; width > 1; width >>= 1)
-      for (int w = 0; w < width / 2; ++w) {
-        s_d[w] = __dadd_rn(s_d[2 * w], s_d[2 * w + 1]);
-        s_d[32 + w] = __dadd_rn(s_d[32 + 2 * w], s_d[32 + 2 * w + 1]);
-        s_d[64 + w] = __dadd_rn(s_d[64 + 2 * w], s_d[64 + 2 * w + 1]);
-      }
-    const double D = s_d[64];
-    double ex = __ddiv_rn(s_d[0], D);
-    double ey = __ddiv_rn(s_d[32], D);
-    if constexpr (MODE == M_FP16) {
-      ex = __dmul_rn(ex, 1.0 / 1024.0);
-      ey = __dmul_rn(ey, 1.0 / 1024.0);
+  if (wid == 0) {
+    double vx = lane < nw ? s_d[lane] : 0.0;
+    double vy = lane < nw ? s_d[32 + lane] : 0.0;
+    double vd = lane < nw ? s_d[64 + lane] : 0.0;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      vx = __dadd_rn(vx, __shfl_xor_sync(0xffffffffu, vx, d));
+      vy = __dadd_rn(vy, __shfl_xor_sync(0xffffffffu, vy, d));
+      vd = __dadd_rn(vd, __shfl_xor_sync(0xffffffffu, vd, d));
     }
-    double* tr = a.traj + ((size_t)track * a.traj_stride + a.traj_index) * 2;
-    tr[0] = ex;
-    tr[1] = ey;
-    a.u_out[track] = u;
-    if (!(D > 0.0) || !isfinite(D) || !isfinite(ex) || !isfinite(ey)) atomicMin(a.degenerate + track, a.t);
+    if (lane == 0) {
+      double ex = __ddiv_rn(vx, vd);
+      double ey = __ddiv_rn(vy, vd);
+      if constexpr (MODE == M_FP16) {
+        ex = __dmul_rn(ex, 1.0 / 1024.0);
+        ey = __dmul_rn(ey, 1.0 / 1024.0);
+      }
+      double* tr = a.traj + ((size_t)track * a.traj_stride + a.traj_index) * 2;
+      tr[0] = ex;
+      tr[1] = ey;
+      a.u_out[track] = u;
+      if (!(vd > 0.0) || !isfinite(vd) || !isfinite(ex) || !isfinite(ey)) atomicMin(a.degenerate + track, a.t);
+    }
   }
 }
 

@@ -57,12 +57,14 @@ constexpr int kJumpDigits = 6;
 __constant__ Affine kJump[kJumpDigits][256];
 
 __device__ __forceinline__ uint64_t word_at(uint64_t x0, uint64_t pos) {
+  // kJump[d][0] is the identity, so all six table loads are unconditional and
+  // independent (one memory latency), followed by six dependent mul-adds.
+  Affine f[kJumpDigits];
+#pragma unroll
+  for (int d = 0; d < kJumpDigits; ++d) f[d] = kJump[d][(pos >> (8 * d)) & 0xff];
   uint64_t x = x0;
 #pragma unroll
-  for (int d = 0; d < kJumpDigits; ++d) {
-    unsigned v = (unsigned)((pos >> (8 * d)) & 0xff);
-    if (v) x = apply(kJump[d][v], x);
-  }
+  for (int d = 0; d < kJumpDigits; ++d) x = apply(f[d], x);
   return x;
 }
 
