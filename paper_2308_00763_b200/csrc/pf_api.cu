@@ -152,7 +152,10 @@ struct pf_handle {
   long long* tab_s = nullptr;
   double *tab_O = nullptr, *tab_invM = nullptr, *u = nullptr;
   unsigned long long* x0 = nullptr;
+  unsigned long long* s_frame = nullptr;
   ulonglong2* tj = nullptr;
+  ulonglong2* tt = nullptr;
+  pfr::Affine f2k{1, 0};
   unsigned short* exp16 = nullptr;
   void* zig = nullptr;
   int2* d_offs = nullptr;
@@ -229,7 +232,7 @@ int pf_destroy(pf_handle* h) {
   if (!h) return PF_OK;
   cudaSetDevice(h->device);
   void* ptrs[] = {h->X[0], h->X[1], h->C[0], h->C[1], h->rec_m, h->rec_S, h->rec_X, h->rec_Y, h->tab_s, h->tab_O,
-                  h->tab_invM, h->u, h->x0, h->tj, h->exp16, h->zig, h->d_offs, h->d_plan, h->d_leaves, h->d_frames,
+                  h->tab_invM, h->u, h->x0, h->s_frame, h->tj, h->tt, h->exp16, h->zig, h->d_offs, h->d_plan, h->d_leaves, h->d_frames,
                   h->d_maps, h->d_traj, h->d_degen, h->dbg_anc, h->dbg_L};
   for (void* p : ptrs)
     if (p) cudaFree(p);
@@ -360,6 +363,20 @@ int pf_create(pf_handle** out, const pf_config* cfg) {
   }
   CK(cudack(cudaMalloc(&h->tj, nv * sizeof(ulonglong2)), "tj"));
   CK(cudack(cudaMemcpy(h->tj, tj.data(), nv * sizeof(ulonglong2), cudaMemcpyHostToDevice), "tj"));
+  // per-tile jumps f^(2 * tile * PF_TILE) and f^(2K)
+  {
+    std::vector<ulonglong2> tt(h->n_tiles);
+    const pfr::Affine step = pfr::affine_pow(2ULL * PF_TILE);
+    pfr::Affine f{1, 0};
+    for (int b = 0; b < h->n_tiles; ++b) {
+      tt[b] = make_ulonglong2(f.a, f.c);
+      f = pfr::compose(step, f);
+    }
+    CK(cudack(cudaMalloc(&h->tt, h->n_tiles * sizeof(ulonglong2)), "tt"));
+    CK(cudack(cudaMemcpy(h->tt, tt.data(), h->n_tiles * sizeof(ulonglong2), cudaMemcpyHostToDevice), "tt"));
+    h->f2k = pfr::affine_pow(2ULL * (unsigned long long)h->K);
+    CK(cudack(cudaMalloc(&h->s_frame, h->n_tracks * 8), "s_frame"));
+  }
   // exp16 table
   std::vector<uint16_t> ex(65536);
   build_exp16(ex.data());
@@ -512,6 +529,8 @@ static int launch_frame(pf_handle* h, const void* map_slot, long long map_video_
   a.dbg_anc = h->dbg_anc;
   a.dbg_L = h->dbg_L;
   a.zig = h->zig;
+  a.s_frame = h->s_frame;
+  a.tt = h->tt;
   dim3 grid(h->n_tiles, h->n_tracks);
   fused_kernel(h)<<<grid, h->tpb, h->fused_smem, h->stream>>>(a);
   PF_CUDA(cudaGetLastError(), h->err);
@@ -531,6 +550,9 @@ static int launch_frame(pf_handle* h, const void* map_slot, long long map_video_
   t.tab_O = h->tab_O;
   t.tab_invM = h->tab_invM;
   t.u_out = h->u;
+  t.s_frame = h->s_frame;
+  t.f2k_a = h->f2k.a;
+  t.f2k_c = h->f2k.c;
   t.traj = h->d_traj;
   t.traj_stride = traj_stride;
   t.traj_index = traj_index;

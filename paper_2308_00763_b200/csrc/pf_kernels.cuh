@@ -302,6 +302,8 @@ struct FusedArgs {
   long long* dbg_anc;  // optional
   void* dbg_L;         // optional
   const void* zig;     // packed ziggurat fast-path tables: ki>>20 (u32 x 256) then wi (f64 x 256)
+  const unsigned long long* s_frame;  // per track: stream state at position t(2K+1) (t > 0)
+  const ulonglong2* tt;               // per tile: f^(2 * tile * PF_TILE)
 };
 
 template <typename T>
@@ -578,11 +580,13 @@ __device__ __forceinline__ int advance_key(const typename Tr<MODE>::real* c, int
   return gallop_key<MODE>(c, j0, n, kq);
 }
 
+// store one component of a particle's noise pair; a plain component store (no
+// read-modify-write of the pair: x and y of one particle may both take the
+// slow path and be written by different threads concurrently)
 template <int MODE>
 __device__ __forceinline__ void set_comp(typename Tr<MODE>::vec& v, int comp, double x) {
   if constexpr (MODE == M_FP16) {
-    const __half h = __double2half(x);
-    v = comp ? __halves2half2(__low2half(v), h) : __halves2half2(h, __high2half(v));
+    reinterpret_cast<__half*>(&v)[comp] = __double2half(x);
   } else {
     if (comp)
       v.y = (typename Tr<MODE>::real)x;
@@ -646,12 +650,14 @@ __global__ void __launch_bounds__(PF_TILE / VPT) pf_fused_frame(FusedArgs a) {
     for (int i = tid; i < 192; i += TPB) zdst[i] = zsrc[i];
   }
   if (tid == 0) {
-    const unsigned long long pos =
-        (unsigned long long)a.t * (unsigned long long)(2 * K + 1) + 2ULL * (unsigned long long)base;
-    s_state[0] = pfr::word_at(a.x0[track], pos);
     s_int[3] = 0;  // slow-path queue counters (alternate per round)
     s_int[4] = 0;
   }
+  // stream state at this tile's first draw, position t(2K+1) + 2*base: the
+  // frame base state (written by the previous frame's tile table) advanced by
+  // the per-tile jump -- two loads and one mul-add, no serial jump-ahead
+  const unsigned long long tstate = pfr::apply(pfr::Affine{a.tt[tile].x, a.tt[tile].y},
+                                               a.t == 0 ? a.x0[track] : a.s_frame[track]);
   // ---- source window of this tile's outputs (previous frame's table) ----
   if (a.t > 0 && wid == 0) {
     const long long kf = base, kl = base + Tb - 1;
@@ -694,7 +700,6 @@ __global__ void __launch_bounds__(PF_TILE / VPT) pf_fused_frame(FusedArgs a) {
     }
   }
   __syncthreads();
-  const unsigned long long tstate = s_state[0];
   int b_lo = 0, b_hi = 0, staged = 0;
   if (a.t > 0) {
     b_lo = s_int[0];
@@ -1055,6 +1060,8 @@ struct TableArgs {
   double* tab_O;
   double* tab_invM;
   double* u_out;
+  unsigned long long* s_frame;  // out: per-track stream state at position (t+1)(2K+1)
+  unsigned long long f2k_a, f2k_c;  // f^(2K)
   double* traj;       // [track][F][2]
   int traj_stride;    // frames per track in traj
   int traj_index;     // frame slot
@@ -1098,12 +1105,13 @@ __global__ void __launch_bounds__(1024) pf_tile_table(TableArgs a) {
   const long long* rX = a.rec_X + (size_t)track * n;
   const long long* rY = a.rec_Y + (size_t)track * n;
 
-  // the frame's resampling uniform (stream position t(2K+1)+2K), computed by
-  // a warp other than warp 0 while the max reduction proceeds
-  if (tid == (nw > 1 ? 32 : 0)) {
-    const unsigned long long pos =
-        (unsigned long long)a.t * (unsigned long long)(2 * a.K + 1) + 2ULL * (unsigned long long)a.K;
-    s_d[97] = pfr::uniform_of(pfr::word_at(a.x0[track], pos));
+  // the frame's resampling uniform: stream position t(2K+1)+2K = f^(2K) of
+  // the frame base state; one more step is the next frame's base state
+  if (tid == 0) {
+    const unsigned long long st = a.t == 0 ? a.x0[track] : a.s_frame[track];
+    const unsigned long long wu = pfr::apply(pfr::Affine{a.f2k_a, a.f2k_c}, st);
+    s_d[97] = pfr::uniform_of(wu);
+    a.s_frame[track] = pfr::kA * wu + pfr::kC;
   }
   // 1. global max (exact)
   double m = __longlong_as_double(0xfff0000000000000LL);

@@ -65,7 +65,7 @@ def test_fused_bitexact_vs_oracle_acceptance(pf, acceptance_video, mode):
 
 
 @pytest.mark.parametrize("mode", ["fp64", "fp32", "fp16"])
-@pytest.mark.parametrize("K", [2, 1023, 1025, 10_000, 40_961])
+@pytest.mark.parametrize("K", [2, 1023, 1025, 10_000, 40_961, 200_003])
 def test_fused_bitexact_vs_oracle_sizes(pf, mode, K):
     frames, _ = rp.generate_video(rp.Params(), 6, 96, 80, (40.0, 30.0), 17)
     traj = pf.Filter(K, mode, 96, 80, 5, start_hint=(40.0, 30.0)).run(frames)
