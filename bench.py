@@ -276,7 +276,13 @@ def main():
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     import paper_2308_00763_b200 as pf
 
-    tracks = max(1, cfg["tracks"] // world) if cfg["tracks"] > 1 else 1
+    from paper_2308_00763_b200.sharding import max_over_ranks, shard_tracks
+
+    # batched independent tracks, block-partitioned over ranks (C2 at N GPUs:
+    # one independent track per rank); global track g -> seed 42+g, video g % nv
+    total_tracks = cfg["tracks"] if cfg["tracks"] > 1 else world
+    shard = shard_tracks(total_tracks, world, rank)
+    tracks = shard.count
     F, K, W, H = cfg["F"], cfg["K"], cfg["W"], cfg["H"]
     nv = cfg["videos"]
     vids, truths = [], []
@@ -284,10 +290,13 @@ def main():
         v = pf.generate_video(pf.ModelParams(), F, W, H, (W / 2.0, H / 2.0), 42 + j)
         vids.append(v.frames)
         truths.append(v.truth)
+    rot = shard.first % nv  # local track i observes video (first + i) % nv
+    vids = vids[rot:] + vids[:rot]
+    truths = truths[rot:] + truths[:rot]
     host_frames = np.ascontiguousarray(np.stack(vids)) if nv > 1 else vids[0]
     dev_frames = torch.from_numpy(host_frames).cuda()
     flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
-    seeds = [42 + rank * tracks + i for i in range(tracks)]
+    seeds = shard.seeds(42)
 
     def make(precision):
         return pf.Filter(K, precision, W, H, seeds=seeds, n_tracks=tracks, n_videos=nv, tpb=args.tpb,
@@ -311,12 +320,8 @@ def main():
             dist.barrier()
         torch.cuda.synchronize()
 
-    def max_over_ranks(x):
-        if dist is None:
-            return x
-        t = torch.tensor([x], dtype=torch.float64, device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        return float(t.item())
+    def over_ranks(x):
+        return max_over_ranks(x, dist, device="cuda")
 
     prec = cfg["precision"]
     f = make(prec)
@@ -331,8 +336,8 @@ def main():
     dev_ms, launches = device_steps(f, args.steps)
     barrier()
     clk = clocks.stop()
-    dev_ms = max_over_ranks(dev_ms)
-    updates_per_step = world * tracks * K * F
+    dev_ms = over_ranks(dev_ms)
+    updates_per_step = total_tracks * K * F
     value = updates_per_step * args.steps / (dev_ms * 1e-3)
     f.reset()
     traj = f.run_frames(dev_frames, F)
@@ -350,7 +355,7 @@ def main():
         f.run_frames(host_frames, F)
         e2e_s += time.perf_counter() - t0
     barrier()
-    e2e_s = max_over_ranks(e2e_s)
+    e2e_s = over_ranks(e2e_s)
     e2e = {"value": updates_per_step * args.steps / e2e_s, "unit": UNIT,
            "h2d_bytes_per_step": int(host_frames.nbytes), "d2h_bytes_per_step": int(tracks * F * 2 * 8),
            "ms_per_step": 1e3 * e2e_s / args.steps, "timer": "wall clock around pf_run (host frames)"}
@@ -391,7 +396,7 @@ def main():
             g = make(p2)
             device_steps(g, 2)
             ms2, _ = device_steps(g, max(3, args.steps // 2))
-            ms2 = max_over_ranks(ms2)
+            ms2 = over_ranks(ms2)
             v2 = updates_per_step * max(3, args.steps // 2) / (ms2 * 1e-3)
             g.reset()
             t2 = g.run_frames(dev_frames, F)
