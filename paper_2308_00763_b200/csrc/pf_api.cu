@@ -152,10 +152,9 @@ struct pf_handle {
   long long* tab_s = nullptr;
   double *tab_O = nullptr, *tab_invM = nullptr, *u = nullptr;
   unsigned long long* x0 = nullptr;
-  unsigned long long* s_frame = nullptr;
   ulonglong2* tj = nullptr;
   ulonglong2* tt = nullptr;
-  pfr::Affine f2k{1, 0};
+  bool pdl = true;
   unsigned short* exp16 = nullptr;
   void* zig = nullptr;
   int2* d_offs = nullptr;
@@ -190,20 +189,42 @@ struct pf_handle {
 };
 
 typedef void (*fused_fn)(pfk::FusedArgs);
+// (VPT, rounds) per threads-per-block: the tile is always PF_TILE particles
 template <int M>
-static fused_fn fused_for_vpt(int vpt) {
-  switch (vpt) {
-    case 1: return pfk::pf_fused_frame<M, 1>;
-    case 2: return pfk::pf_fused_frame<M, 2>;
-    case 4: return pfk::pf_fused_frame<M, 4>;
-    default: return pfk::pf_fused_frame<M, 8>;
+static fused_fn fused_for_tpb(int tpb) {
+  switch (tpb) {
+    case 32: return pfk::pf_fused_frame<M, 8, 4>;
+    case 64: return pfk::pf_fused_frame<M, 8, 2>;
+    case 128: return pfk::pf_fused_frame<M, 8, 1>;
+    case 512: return pfk::pf_fused_frame<M, 2, 1>;
+    case 1024: return pfk::pf_fused_frame<M, 1, 1>;
+    default: return pfk::pf_fused_frame<M, 4, 1>;
   }
 }
 static fused_fn fused_kernel(const pf_handle* h) {
-  return h->km == 0 ? fused_for_vpt<0>(h->vpt) : h->km == 1 ? fused_for_vpt<1>(h->vpt) : fused_for_vpt<2>(h->vpt);
+  return h->km == 0 ? fused_for_tpb<0>(h->tpb) : h->km == 1 ? fused_for_tpb<1>(h->tpb) : fused_for_tpb<2>(h->tpb);
 }
 static cudaError_t set_fused_smem(const pf_handle* h) {
   return cudaFuncSetAttribute(fused_kernel(h), cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->fused_smem);
+}
+
+// launch with programmatic stream serialization (PDL): the kernel may begin
+// before its predecessor finishes and waits (griddepcontrol.wait) where it
+// consumes the predecessor's results
+template <typename Args>
+static cudaError_t launch_pdl(const pf_handle* h, const void* fn, dim3 grid, dim3 block, size_t smem, Args args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = h->stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = h->pdl ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  void* params[1] = {&args};
+  return cudaLaunchKernelExC(&cfg, fn, params);
 }
 
 static int grow(void** p, size_t* cap, size_t bytes, std::string& err) {
@@ -232,7 +253,7 @@ int pf_destroy(pf_handle* h) {
   if (!h) return PF_OK;
   cudaSetDevice(h->device);
   void* ptrs[] = {h->X[0], h->X[1], h->C[0], h->C[1], h->rec_m, h->rec_S, h->rec_X, h->rec_Y, h->tab_s, h->tab_O,
-                  h->tab_invM, h->u, h->x0, h->s_frame, h->tj, h->tt, h->exp16, h->zig, h->d_offs, h->d_plan, h->d_leaves, h->d_frames,
+                  h->tab_invM, h->u, h->x0, h->tj, h->tt, h->exp16, h->zig, h->d_offs, h->d_plan, h->d_leaves, h->d_frames,
                   h->d_maps, h->d_traj, h->d_degen, h->dbg_anc, h->dbg_L};
   for (void* p : ptrs)
     if (p) cudaFree(p);
@@ -374,8 +395,6 @@ int pf_create(pf_handle** out, const pf_config* cfg) {
     }
     CK(cudack(cudaMalloc(&h->tt, h->n_tiles * sizeof(ulonglong2)), "tt"));
     CK(cudack(cudaMemcpy(h->tt, tt.data(), h->n_tiles * sizeof(ulonglong2), cudaMemcpyHostToDevice), "tt"));
-    h->f2k = pfr::affine_pow(2ULL * (unsigned long long)h->K);
-    CK(cudack(cudaMalloc(&h->s_frame, h->n_tracks * 8), "s_frame"));
   }
   // exp16 table
   std::vector<uint16_t> ex(65536);
@@ -529,10 +548,12 @@ static int launch_frame(pf_handle* h, const void* map_slot, long long map_video_
   a.dbg_anc = h->dbg_anc;
   a.dbg_L = h->dbg_L;
   a.zig = h->zig;
-  a.s_frame = h->s_frame;
+  const pfr::Affine ff = pfr::affine_pow((unsigned long long)h->frame_counter * (2ULL * h->K + 1));
+  a.fa = ff.a;
+  a.fc = ff.c;
   a.tt = h->tt;
-  dim3 grid(h->n_tiles, h->n_tracks);
-  fused_kernel(h)<<<grid, h->tpb, h->fused_smem, h->stream>>>(a);
+  PF_CUDA(launch_pdl(h, (const void*)fused_kernel(h), dim3(h->n_tiles, h->n_tracks), dim3(h->tpb), h->fused_smem, a),
+          h->err);
   PF_CUDA(cudaGetLastError(), h->err);
   if (h->profiling) PF_CUDA(cudaEventRecord(h->pev[3 * traj_index + 1], h->stream), h->err);
   pfk::TableArgs t{};
@@ -550,20 +571,17 @@ static int launch_frame(pf_handle* h, const void* map_slot, long long map_video_
   t.tab_O = h->tab_O;
   t.tab_invM = h->tab_invM;
   t.u_out = h->u;
-  t.s_frame = h->s_frame;
-  t.f2k_a = h->f2k.a;
-  t.f2k_c = h->f2k.c;
+  const pfr::Affine fu =
+      pfr::affine_pow((unsigned long long)h->frame_counter * (2ULL * h->K + 1) + 2ULL * (unsigned long long)h->K);
+  t.ua = fu.a;
+  t.uc = fu.c;
   t.traj = h->d_traj;
   t.traj_stride = traj_stride;
   t.traj_index = traj_index;
   t.degenerate = h->d_degen;
-  const size_t tsm = 0;
-  if (h->km == 0)
-    pfk::pf_tile_table<0><<<h->n_tracks, h->tpb_table, tsm, h->stream>>>(t);
-  else if (h->km == 1)
-    pfk::pf_tile_table<1><<<h->n_tracks, h->tpb_table, tsm, h->stream>>>(t);
-  else
-    pfk::pf_tile_table<2><<<h->n_tracks, h->tpb_table, tsm, h->stream>>>(t);
+  const void* tk = h->km == 0 ? (const void*)pfk::pf_tile_table<0>
+                   : h->km == 1 ? (const void*)pfk::pf_tile_table<1> : (const void*)pfk::pf_tile_table<2>;
+  PF_CUDA(launch_pdl(h, tk, dim3(h->n_tracks), dim3(h->tpb_table), 0, t), h->err);
   PF_CUDA(cudaGetLastError(), h->err);
   if (h->profiling) PF_CUDA(cudaEventRecord(h->pev[3 * traj_index + 2], h->stream), h->err);
   h->launches += 2;

@@ -302,9 +302,15 @@ struct FusedArgs {
   long long* dbg_anc;  // optional
   void* dbg_L;         // optional
   const void* zig;     // packed ziggurat fast-path tables: ki>>20 (u32 x 256) then wi (f64 x 256)
-  const unsigned long long* s_frame;  // per track: stream state at position t(2K+1) (t > 0)
-  const ulonglong2* tt;               // per tile: f^(2 * tile * PF_TILE)
+  unsigned long long fa, fc;  // f^(t(2K+1)): frame base state = fa * x0[track] + fc
+  const ulonglong2* tt;       // per tile: f^(2 * tile * PF_TILE)
 };
+
+// Programmatic dependent launch: let the next kernel in the stream start
+// early, and wait for the previous kernel's results only where they are
+// consumed (no-ops when launched without the PDL attribute).
+__device__ __forceinline__ void pdl_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 
 template <typename T>
 __device__ __forceinline__ T shfl_up(T v, int d) {
@@ -542,23 +548,23 @@ __device__ __forceinline__ typename Tr<MODE>::vec prop(typename Tr<MODE>::vec xa
 
 template <int MODE>
 constexpr int max_src_tiles() {
-  return MODE == M_FP64 ? 3 : (MODE == M_FP32 ? 6 : 12);
+  return MODE == M_FP64 ? 2 : (MODE == M_FP32 ? 4 : 6);
 }
 
-constexpr int kSlowQ = 256;  // deferred ziggurat slow paths per CTA (overflow -> inline)
+constexpr int kSlowQ = 128;  // deferred ziggurat slow paths per CTA (overflow -> inline)
 
 template <int MODE>
 constexpr size_t fused_smem_bytes() {
   using real = typename Tr<MODE>::real;
   using vec = typename Tr<MODE>::vec;
-  return 4096 + PF_TILE * (sizeof(real) + sizeof(vec)) + max_src_tiles<MODE>() * PF_TILE * sizeof(real) +
-         (max_src_tiles<MODE>() + 1) * 24 + kSlowQ * 16 + 256 * 8;
+  return 3072 + PF_TILE * (sizeof(real) + sizeof(vec)) + max_src_tiles<MODE>() * PF_TILE * sizeof(real) +
+         (max_src_tiles<MODE>() + 1) * 24 + kSlowQ * 12 + 320 * 8;
 }
 
 // branchless lower bound: first j in [0, n) with key(c[j]) >= kq, n if none
 template <int MODE>
 __device__ __forceinline__ int lb_branchless(const typename Tr<MODE>::real* c, int n, typename Key<MODE>::k_t kq) {
-  int lo = 0;  // invariant: answer in [lo, lo + len]
+  int lo = 0;
   int len = n;
   while (len > 0) {
     const int half = len >> 1;
@@ -580,9 +586,9 @@ __device__ __forceinline__ int advance_key(const typename Tr<MODE>::real* c, int
   return gallop_key<MODE>(c, j0, n, kq);
 }
 
-// store one component of a particle's noise pair; a plain component store (no
-// read-modify-write of the pair: x and y of one particle may both take the
-// slow path and be written by different threads concurrently)
+// store one component of a particle's noise pair: a plain component store
+// (x and y of one particle may both take the slow path and be written by
+// different threads concurrently -- no read-modify-write of the pair)
 template <int MODE>
 __device__ __forceinline__ void set_comp(typename Tr<MODE>::vec& v, int comp, double x) {
   if constexpr (MODE == M_FP16) {
@@ -595,79 +601,130 @@ __device__ __forceinline__ void set_comp(typename Tr<MODE>::vec& v, int comp, do
   }
 }
 
-template <int MODE, int VPT>
-__global__ void __launch_bounds__(PF_TILE / VPT) pf_fused_frame(FusedArgs a) {
+// canonical pairwise tree over a thread's VPT consecutive values
+template <int VPT>
+__device__ __forceinline__ double tree_vpt(const double* v) {
+  if constexpr (VPT == 8)
+    return __dadd_rn(__dadd_rn(__dadd_rn(v[0], v[1]), __dadd_rn(v[2], v[3])),
+                     __dadd_rn(__dadd_rn(v[4], v[5]), __dadd_rn(v[6], v[7])));
+  else if constexpr (VPT == 4)
+    return __dadd_rn(__dadd_rn(v[0], v[1]), __dadd_rn(v[2], v[3]));
+  else if constexpr (VPT == 2)
+    return __dadd_rn(v[0], v[1]);
+  else
+    return v[0];
+}
+
+// One CTA = one tile of PF_TILE particles of one track; TPB = PF_TILE/(VPT*R)
+// threads, thread t of round r owns particles (r*TPB + t)*VPT .. +VPT-1.
+template <int MODE, int VPT, int R>
+__global__ void __launch_bounds__(PF_TILE / (VPT * R)) pf_fused_frame(FusedArgs a) {
   using real = typename Tr<MODE>::real;
   using vec = typename Tr<MODE>::vec;
   using wq_t = typename Tr<MODE>::wq_t;
   using KT = Key<MODE>;
   constexpr int MS = max_src_tiles<MODE>();
+  constexpr int TPB = PF_TILE / (VPT * R);
+  constexpr int NW = TPB / 32;
   extern __shared__ __align__(16) unsigned char smem[];
   uint32_t* s_kihi = reinterpret_cast<uint32_t*>(smem);   // 1 KB
   double* s_wi = reinterpret_cast<double*>(smem + 1024);  // 2 KB
-  real* s_L = reinterpret_cast<real*>(smem + 4096);
-  vec* s_X = reinterpret_cast<vec*>(smem + 4096 + PF_TILE * sizeof(real));  // normals, then positions, then cum
-  real* s_c = reinterpret_cast<real*>(smem + 4096 + PF_TILE * (sizeof(real) + sizeof(vec)));
+  real* s_L = reinterpret_cast<real*>(smem + 3072);       // R > 1 only
+  vec* s_X = reinterpret_cast<vec*>(smem + 3072 + PF_TILE * sizeof(real));  // noise, then positions (R > 1)
+  real* s_c = reinterpret_cast<real*>(smem + 3072 + PF_TILE * (sizeof(real) + sizeof(vec)));
   unsigned char* p_tab = reinterpret_cast<unsigned char*>(s_c + MS * PF_TILE);
-  long long* s_ts = reinterpret_cast<long long*>(p_tab);           // MS + 1
+  int* s_ts = reinterpret_cast<int*>(p_tab);                        // MS + 1 (in-track indices)
   double* s_tO = reinterpret_cast<double*>(p_tab + (MS + 1) * 8);   // MS + 1
   double* s_tM = reinterpret_cast<double*>(p_tab + (MS + 1) * 16);  // MS + 1
   unsigned long long* s_qw = reinterpret_cast<unsigned long long*>(p_tab + (MS + 1) * 24);
   int* s_qs = reinterpret_cast<int*>(s_qw + kSlowQ);
-  unsigned char* s_misc = reinterpret_cast<unsigned char*>(s_qs + 2 * kSlowQ);
-  long long* s_red = reinterpret_cast<long long*>(s_misc);        // 64
-  double* s_redd = reinterpret_cast<double*>(s_misc + 64 * 8);    // 32
-  double* s_wx = reinterpret_cast<double*>(s_misc + 96 * 8);      // 32
-  double* s_wy = reinterpret_cast<double*>(s_misc + 128 * 8);     // 32
-  double* s_round = reinterpret_cast<double*>(s_misc + 160 * 8);  // 64
-  unsigned long long* s_state = reinterpret_cast<unsigned long long*>(s_misc + 224 * 8);
-  int* s_int = reinterpret_cast<int*>(s_misc + 225 * 8);  // b_lo, b_hi, staged, queue count
-  real* s_m = reinterpret_cast<real*>(s_misc + 228 * 8);
+  double* s_misc = reinterpret_cast<double*>(s_qs + kSlowQ);
+  // misc (8-byte slots): [0..31] warp max, [32..63] warp totals, [64..95] / [96..127] warp moments,
+  // [128..191] round moments, [192..199] ints
+  long long* s_wtot = reinterpret_cast<long long*>(s_misc + 32);
+  int* s_int = reinterpret_cast<int*>(s_misc + 192);  // b_lo, b_hi, staged, queue count
 
-  const int TPB = blockDim.x;
-  const int R = PF_TILE / (TPB * VPT);
-  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, nw = TPB >> 5;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const int tile = blockIdx.x, track = blockIdx.y;
-  const long long K = a.K;
-  const long long base = (long long)tile * PF_TILE;
-  const int Tb = (int)min((long long)PF_TILE, K - base);
+  const int K = (int)a.K;
+  const int base = tile * PF_TILE;
+  const int Tb = min(PF_TILE, K - base);
   const int n = a.n_tiles;
 
-  const vec* Xp = reinterpret_cast<const vec*>(a.X_prev) + (size_t)track * K;
-  vec* Xn = reinterpret_cast<vec*>(a.X_new) + (size_t)track * K;
-  const real* Cp = reinterpret_cast<const real*>(a.C_prev) + (size_t)track * K;
-  real* Cn = reinterpret_cast<real*>(a.C_new) + (size_t)track * K;
-  const real* map = reinterpret_cast<const real*>(a.map) + (size_t)(track % a.n_videos) * a.map_video_stride;
+  const vec* __restrict__ Xp = reinterpret_cast<const vec*>(a.X_prev) + (size_t)track * K;
+  vec* __restrict__ Xn = reinterpret_cast<vec*>(a.X_new) + (size_t)track * K;
+  const real* __restrict__ Cp = reinterpret_cast<const real*>(a.C_prev) + (size_t)track * K;
+  real* __restrict__ Cn = reinterpret_cast<real*>(a.C_new) + (size_t)track * K;
+  const real* __restrict__ map = reinterpret_cast<const real*>(a.map) + (size_t)(track % a.n_videos) * a.map_video_stride;
   const long long* ts = a.tab_s + (size_t)track * n;
   const double* tO = a.tab_O + (size_t)track * n;
   const double* tM = a.tab_invM + (size_t)track * n;
-  const double u = a.t > 0 ? a.u_prev[track] : 0.0;
-  const double invK = __ddiv_rn(1.0, __ll2double_rn(K));
 
   {
-    const uint4* zsrc = reinterpret_cast<const uint4*>(a.zig);  // {ki_hi x4} / {wi x2} packed 16 B
+    const uint4* zsrc = reinterpret_cast<const uint4*>(a.zig);
     uint4* zdst = reinterpret_cast<uint4*>(smem);
     for (int i = tid; i < 192; i += TPB) zdst[i] = zsrc[i];
   }
-  if (tid == 0) {
-    s_int[3] = 0;  // slow-path queue counters (alternate per round)
-    s_int[4] = 0;
-  }
+  if (tid == 0) s_int[3] = 0;
   // stream state at this tile's first draw, position t(2K+1) + 2*base: the
-  // frame base state (written by the previous frame's tile table) advanced by
-  // the per-tile jump -- two loads and one mul-add, no serial jump-ahead
-  const unsigned long long tstate = pfr::apply(pfr::Affine{a.tt[tile].x, a.tt[tile].y},
-                                               a.t == 0 ? a.x0[track] : a.s_frame[track]);
-  // ---- source window of this tile's outputs (previous frame's table) ----
-  if (a.t > 0 && wid == 0) {
-    const long long kf = base, kl = base + Tb - 1;
+  // frame's affine jump (kernel argument) and the per-tile jump
+  const unsigned long long tstate =
+      pfr::apply(pfr::Affine{a.tt[tile].x, a.tt[tile].y}, a.fa * a.x0[track] + a.fc);
+  pdl_launch_dependents();
+  __syncthreads();
+
+  // ---- phase 0: every draw of the tile (independent of the previous frame:
+  // overlaps the previous kernel under PDL).  Fast ziggurat path into s_X as
+  // mode-dtype noise; slow paths queued, resolved in one CTA-wide pass.
+#pragma unroll
+  for (int rr = 0; rr < R; ++rr) {
+    const int v = rr * TPB + tid;
+    const int l0 = v * VPT;
+    unsigned long long xs = pfr::apply(pfr::Affine{a.tj[v].x, a.tj[v].y}, tstate);
+#pragma unroll
+    for (int i = 0; i < VPT; ++i) {
+      double nn[2];
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
+        const unsigned long long w = xs;
+        xs = pfr::kA * xs + pfr::kC;
+        const unsigned idx = (unsigned)(w >> 56);
+        const unsigned long long rabs = (w >> 3) & pfr::kMask52;
+        const double x = __dmul_rn((double)rabs, s_wi[idx]);
+        nn[c] = ((w >> 55) & 1) ? -x : x;
+        if ((unsigned)(rabs >> 20) >= s_kihi[idx] && l0 + i < Tb) {
+          const int slot = atomicAdd(&s_int[3], 1);
+          if (slot < kSlowQ) {
+            s_qw[slot] = w;
+            s_qs[slot] = (l0 + i) * 2 + c;
+          } else {
+            nn[c] = pfr::zig_slow(w);  // queue overflow (never in practice)
+          }
+        }
+      }
+      s_X[l0 + i] = to_vec<MODE>(nn[0], nn[1]);
+    }
+  }
+  __syncthreads();
+  {
+    const int nq = min(s_int[3], kSlowQ);
+    for (int e = tid; e < nq; e += TPB) {
+      const int sl = s_qs[e];
+      set_comp<MODE>(s_X[sl >> 1], sl & 1, pfr::zig_slow(s_qw[e]));
+    }
+  }
+  // ---- everything below consumes the previous kernels' results ----------
+  pdl_wait();
+  const double u = a.t > 0 ? a.u_prev[track] : 0.0;
+  if (a.t > 0 && wid == 0) {  // source window: last tile with s_b <= first / last output
+    const int kf = base, kl = base + Tb - 1;
     const int w0 = max(0, min(tile - 16, n - 32));
     const int bw = min(w0 + lane, n - 1);
-    const long long sv = __ldg(ts + bw);
+    const int sv = (int)__ldg(ts + bw);
     int res[2];
 #pragma unroll
     for (int e = 0; e < 2; ++e) {
-      const long long kk = e == 0 ? kf : kl;
+      const int kk = e == 0 ? kf : kl;
       const unsigned ball = __ballot_sync(0xffffffffu, sv <= kk);
       const int topb = min(w0 + 31, n - 1);
       int b = -1;
@@ -676,7 +733,7 @@ __global__ void __launch_bounds__(PF_TILE / VPT) pf_fused_frame(FusedArgs a) {
         int lo = 0, hi = n - 1;
         while (lo < hi) {
           const int mid = (lo + hi + 1) >> 1;
-          if (__ldg(ts + mid) <= kk)
+          if ((int)__ldg(ts + mid) <= kk)
             lo = mid;
           else
             hi = mid - 1;
@@ -694,25 +751,25 @@ __global__ void __launch_bounds__(PF_TILE / VPT) pf_fused_frame(FusedArgs a) {
     }
     if (staged && lane <= nsrc) {
       const int b = min(res[0] + lane, n - 1);
-      s_ts[lane] = lane < nsrc ? __ldg(ts + b) : K;
+      s_ts[lane] = lane < nsrc ? (int)__ldg(ts + b) : K;
       s_tO[lane] = __ldg(tO + b);
       s_tM[lane] = __ldg(tM + b);
     }
   }
-  __syncthreads();
+  __syncthreads();  // window + slow-path noise visible
   int b_lo = 0, b_hi = 0, staged = 0;
   if (a.t > 0) {
     b_lo = s_int[0];
     b_hi = s_int[1];
     staged = s_int[2];
     if (staged) {  // 16-byte copies of the source tiles' local CDFs
-      const long long c0 = (long long)b_lo * PF_TILE;
-      const int cnt = (int)(min((long long)(b_hi + 1) * PF_TILE, K) - c0);
+      const int c0 = b_lo * PF_TILE;
+      const int cnt = min((b_hi + 1) * PF_TILE, K) - c0;
       constexpr int PER = 16 / sizeof(real);
-      const int nvec = cnt / PER;
-      const uint4* src = reinterpret_cast<const uint4*>(Cp + c0);
-      uint4* dst = reinterpret_cast<uint4*>(s_c);
       if ((((size_t)track * K) % PER) == 0) {
+        const int nvec = cnt / PER;
+        const uint4* src = reinterpret_cast<const uint4*>(Cp + c0);
+        uint4* dst = reinterpret_cast<uint4*>(s_c);
         for (int i = tid; i < nvec; i += TPB) dst[i] = __ldg(src + i);
         for (int i = nvec * PER + tid; i < cnt; i += TPB) s_c[i] = Cp[c0 + i];
       } else {
@@ -721,10 +778,8 @@ __global__ void __launch_bounds__(PF_TILE / VPT) pf_fused_frame(FusedArgs a) {
       __syncthreads();
     }
   }
-  const long long* Ts = staged ? s_ts - b_lo : ts;
-  const double* TO = staged ? s_tO - b_lo : tO;
-  const double* TM = staged ? s_tM - b_lo : tM;
-  const real* Csrc = staged ? s_c - (long long)b_lo * PF_TILE : Cp;
+  const real* Csrc = staged ? s_c - b_lo * PF_TILE : Cp;
+  const double invK = __ddiv_rn(1.0, (double)K);
 
   vec drift, stdv;
   if constexpr (MODE == M_FP16) {
@@ -736,63 +791,28 @@ __global__ void __launch_bounds__(PF_TILE / VPT) pf_fused_frame(FusedArgs a) {
     stdv.x = (real)a.std_x;
     stdv.y = (real)a.std_y;
   }
+  auto tab_s = [&](int b) -> int { return staged ? s_ts[b - b_lo] : (int)__ldg(ts + b); };
+  auto tab_O = [&](int b) -> double { return staged ? s_tO[b - b_lo] : __ldg(tO + b); };
+  auto tab_M = [&](int b) -> double { return staged ? s_tM[b - b_lo] : __ldg(tM + b); };
 
-  // ---------------- phase 1: resample + propagate + likelihood ----------
+  // ---- phase 1: resample + propagate + likelihood -------------------------
+  real Lr[R][VPT];
+  vec Xr[R][VPT];
   real tmax = neg_inf<MODE>();
+#pragma unroll
   for (int rr = 0; rr < R; ++rr) {
-    const int v = rr * TPB + tid;
-    const int l0 = v * VPT;
-    const long long k0 = base + l0;
-    // (a) draws: fast ziggurat path into s_X (as mode-dtype noise); slow
-    //     paths queued for one CTA-wide pass
-    {
-      unsigned long long xs = pfr::apply(pfr::Affine{a.tj[v].x, a.tj[v].y}, tstate);
-#pragma unroll
-      for (int i = 0; i < VPT; ++i) {
-        double nn[2];
-#pragma unroll
-        for (int c = 0; c < 2; ++c) {
-          const unsigned long long w = xs;
-          xs = pfr::kA * xs + pfr::kC;
-          const unsigned idx = (unsigned)(w >> 56);
-          const unsigned long long rabs = (w >> 3) & pfr::kMask52;
-          const double x = __dmul_rn((double)rabs, s_wi[idx]);
-          nn[c] = ((w >> 55) & 1) ? -x : x;
-          if ((unsigned)(rabs >> 20) >= s_kihi[idx] && l0 + i < Tb) {
-            const int slot = atomicAdd(&s_int[3 + (rr & 1)], 1);
-            if (slot < kSlowQ) {
-              s_qw[slot] = w;
-              s_qs[slot] = (l0 + i) * 2 + c;
-            } else {
-              nn[c] = pfr::zig_slow(w);  // queue overflow (never in practice)
-            }
-          }
-        }
-        s_X[l0 + i] = to_vec<MODE>(nn[0], nn[1]);
-      }
-    }
-    __syncthreads();
-    {
-      const int nq = min(s_int[3 + (rr & 1)], kSlowQ);
-      for (int e = tid; e < nq; e += TPB) {
-        const int sl = s_qs[e];
-        set_comp<MODE>(s_X[sl >> 1], sl & 1, pfr::zig_slow(s_qw[e]));
-      }
-    }
-    __syncthreads();
-    if (tid == 0) s_int[3 + (rr & 1)] = 0;  // reused by round rr + 2, after round rr + 1's barriers
-    // (b) ancestors
-    long long anc[VPT];
+    const int l0 = (rr * TPB + tid) * VPT;
+    int anc[VPT];
     if (a.t == 0 || l0 >= Tb) {
 #pragma unroll
-      for (int i = 0; i < VPT; ++i) anc[i] = k0 + i;
+      for (int i = 0; i < VPT; ++i) anc[i] = base + l0 + i;
     } else {
       int b = b_lo;
       if (!staged) {
         int lo = b_lo, hi = b_hi;
         while (lo < hi) {
           const int mid = (lo + hi + 1) >> 1;
-          if (__ldg(ts + mid) <= k0)
+          if ((int)__ldg(ts + mid) <= base + l0)
             lo = mid;
           else
             hi = mid - 1;
@@ -802,25 +822,25 @@ __global__ void __launch_bounds__(PF_TILE / VPT) pf_fused_frame(FusedArgs a) {
       int jprev = 0, bprev = -1;
 #pragma unroll
       for (int i = 0; i < VPT; ++i) {
-        const long long k = k0 + i;
+        const int k = base + l0 + i;
         if (k >= K) {
           anc[i] = k;
           continue;
         }
-        while (b < b_hi && Ts[b + 1] <= k) ++b;
+        while (b < b_hi && tab_s(b + 1) <= k) ++b;
         typename KT::k_t kq;
         if constexpr (MODE == M_FP16) {
-          // tile-local point: q = ((k - s_b) + phi_b) * rho_b in f32 (phi, rho from the table)
-          const float qf = __fmul_rn(__fadd_rn((float)(int)(k - Ts[b]), (float)TO[b]), (float)TM[b]);
+          // f32 tile-local point: q = ((k - s_b) + phi_b) * rho_b
+          const float qf = __fmul_rn(__fadd_rn((float)(k - tab_s(b)), (float)tab_O(b)), (float)tab_M(b));
           kq = __half_as_ushort(__float2half_ru(fminf(fmaxf(qf, 0.0f), 1.0f)));
         } else {
           const double p = point_of<MODE>(k, u, K, invK);
-          const double im = TM[b];
-          double q = im == 0.0 ? 0.0 : __dmul_rn(__dsub_rn(p, TO[b]), im);
+          const double im = tab_M(b);
+          const double q = im == 0.0 ? 0.0 : __dmul_rn(__dsub_rn(p, tab_O(b)), im);
           kq = KT::up(fmin(fmax(q, 0.0), 1.0));
         }
-        const long long tl = (long long)b * PF_TILE;
-        const int tb = (int)min((long long)PF_TILE, K - tl);
+        const int tl = b * PF_TILE;
+        const int tb = min(PF_TILE, K - tl);
         const real* cb = Csrc + tl;
         int j = (b == bprev) ? advance_key<MODE>(cb, jprev, tb, kq) : lb_branchless<MODE>(cb, tb, kq);
         j = min(j, tb - 1);
@@ -829,7 +849,6 @@ __global__ void __launch_bounds__(PF_TILE / VPT) pf_fused_frame(FusedArgs a) {
         anc[i] = tl + j;
       }
     }
-    // (c) gather + propagate + likelihood
 #pragma unroll
     for (int i = 0; i < VPT; ++i) {
       const int l = l0 + i;
@@ -839,150 +858,139 @@ __global__ void __launch_bounds__(PF_TILE / VPT) pf_fused_frame(FusedArgs a) {
         const int ix = round_clamp<MODE>(xn.x, -a.r, a.W - 1 + a.r);
         const int iy = round_clamp<MODE>(xn.y, -a.r, a.H - 1 + a.r);
         const real L = map[(iy + a.r) * a.Wm + (ix + a.r)];
-        s_L[l] = L;
-        s_X[l] = xn;
+        Lr[rr][i] = L;
+        Xr[rr][i] = xn;
         if (gt_real<MODE>(L, tmax)) tmax = L;
         if (a.dbg_anc) a.dbg_anc[(size_t)track * K + base + l] = anc[i];
         if (a.dbg_L) reinterpret_cast<real*>(a.dbg_L)[(size_t)track * K + base + l] = L;
       } else {
-        s_L[l] = neg_inf<MODE>();
-        vec z;
-        z.x = (real)0;
-        z.y = (real)0;
-        s_X[l] = z;
+        Lr[rr][i] = neg_inf<MODE>();
+        Xr[rr][i].x = (real)0;
+        Xr[rr][i].y = (real)0;
       }
     }
   }
-  // tile max (exact)
+  // tile max (exact): warp max, one barrier, every thread reduces the NW values
 #pragma unroll
   for (int d = 16; d >= 1; d >>= 1) {
     const real o = __shfl_xor_sync(0xffffffffu, tmax, d);
     if (gt_real<MODE>(o, tmax)) tmax = o;
   }
-  if (lane == 0) reinterpret_cast<real*>(s_redd)[wid] = tmax;
+  if (lane == 0) reinterpret_cast<real*>(s_misc)[wid] = tmax;
   __syncthreads();
-  if (tid == 0) {
-    real mm = reinterpret_cast<real*>(s_redd)[0];
-    for (int w = 1; w < nw; ++w) {
-      const real o = reinterpret_cast<real*>(s_redd)[w];
-      if (gt_real<MODE>(o, mm)) mm = o;
-    }
-    *s_m = mm;
+  real mtile = reinterpret_cast<real*>(s_misc)[0];
+#pragma unroll
+  for (int w = 1; w < NW; ++w) {
+    const real o = reinterpret_cast<real*>(s_misc)[w];
+    if (gt_real<MODE>(o, mtile)) mtile = o;
   }
-  __syncthreads();
-  const real mtile = *s_m;
-  const double mtile_d = to_d(mtile);
 
-  // ---------------- phase 2: weights, exact scan, local cdf, moments ------
-  wq_t carry = 0;
+  // ---- phase 2: weights, exact scan, local cdf, moments --------------------
+  wq_t cum[R][VPT];
+  wq_t thr_tot[R];
   long long mx_i = 0, my_i = 0;
-  wq_t cum_r[VPT];  // R == 1: inclusive cum stays in registers
+  double rmx[R], rmy[R];
+#pragma unroll
   for (int rr = 0; rr < R; ++rr) {
-    const int v = rr * TPB + tid;
-    const int l0 = v * VPT;
-    wq_t wq[VPT];
-    wq_t loc = 0;
+    const int l0 = (rr * TPB + tid) * VPT;
+    wq_t run = 0;
+    double px[VPT], py[VPT];
 #pragma unroll
     for (int i = 0; i < VPT; ++i) {
-      const int l = l0 + i;
-      wq[i] = (l < Tb) ? weight_q<MODE>(s_L[l], mtile, a.exp16) : (wq_t)0;
-      loc += wq[i];
-    }
-    wq_t tot;
-    const wq_t excl = block_excl_scan<wq_t>(loc, reinterpret_cast<wq_t*>(s_red), &tot);
-    double px_d[VPT], py_d[VPT];
-#pragma unroll
-    for (int i = 0; i < VPT; ++i) {
-      const vec xv = s_X[l0 + i];
+      const wq_t w = (l0 + i < Tb) ? weight_q<MODE>(Lr[rr][i], mtile, a.exp16) : (wq_t)0;
+      run += w;
+      cum[rr][i] = run;  // thread-local inclusive
       if constexpr (MODE == M_FP16) {
-        const int xq = __float2int_rn(__fmul_rn(__half2float(xv.x), 1024.0f));
-        const int yq = __float2int_rn(__fmul_rn(__half2float(xv.y), 1024.0f));
-        mx_i += (long long)wq[i] * xq;
-        my_i += (long long)wq[i] * yq;
+        const int xq = __float2int_rn(__fmul_rn(__half2float(Xr[rr][i].x), 1024.0f));
+        const int yq = __float2int_rn(__fmul_rn(__half2float(Xr[rr][i].y), 1024.0f));
+        mx_i += (long long)w * xq;
+        my_i += (long long)w * yq;
       } else {
-        const double w = (double)wq[i];
-        px_d[i] = __dmul_rn(w, to_d(xv.x));
-        py_d[i] = __dmul_rn(w, to_d(xv.y));
+        const double wd = (double)w;
+        px[i] = __dmul_rn(wd, to_d(Xr[rr][i].x));
+        py[i] = __dmul_rn(wd, to_d(Xr[rr][i].y));
       }
     }
-    wq_t run = carry + excl;
-#pragma unroll
-    for (int i = 0; i < VPT; ++i) {
-      run += wq[i];
-      cum_r[i] = run;
-    }
-    if (R > 1) {
-      __syncthreads();  // positions of this round consumed before cum overwrites them
-#pragma unroll
-      for (int i = 0; i < VPT; ++i) reinterpret_cast<wq_t*>(s_X)[l0 + i] = cum_r[i];
-    }
-    carry += tot;
+    thr_tot[rr] = run;
     if constexpr (MODE != M_FP16) {
-      double sx, sy;
-      if constexpr (VPT == 8) {
-        sx = __dadd_rn(__dadd_rn(__dadd_rn(px_d[0], px_d[1]), __dadd_rn(px_d[2], px_d[3])),
-                       __dadd_rn(__dadd_rn(px_d[4], px_d[5]), __dadd_rn(px_d[6], px_d[7])));
-        sy = __dadd_rn(__dadd_rn(__dadd_rn(py_d[0], py_d[1]), __dadd_rn(py_d[2], py_d[3])),
-                       __dadd_rn(__dadd_rn(py_d[4], py_d[5]), __dadd_rn(py_d[6], py_d[7])));
-      } else if constexpr (VPT == 4) {
-        sx = __dadd_rn(__dadd_rn(px_d[0], px_d[1]), __dadd_rn(px_d[2], px_d[3]));
-        sy = __dadd_rn(__dadd_rn(py_d[0], py_d[1]), __dadd_rn(py_d[2], py_d[3]));
-      } else if constexpr (VPT == 2) {
-        sx = __dadd_rn(px_d[0], px_d[1]);
-        sy = __dadd_rn(py_d[0], py_d[1]);
-      } else {
-        sx = px_d[0];
-        sy = py_d[0];
-      }
+      double sx = tree_vpt<VPT>(px), sy = tree_vpt<VPT>(py);
 #pragma unroll
       for (int d = 1; d < 32; d <<= 1) {
         sx = __dadd_rn(sx, __shfl_xor_sync(0xffffffffu, sx, d));
         sy = __dadd_rn(sy, __shfl_xor_sync(0xffffffffu, sy, d));
       }
-      if (lane == 0) {
-        s_wx[wid] = sx;
-        s_wy[wid] = sy;
-      }
-      __syncthreads();
-      if (wid == 0) {  // canonical tree over warps: butterfly with zero padding
-        double wx = lane < nw ? s_wx[lane] : 0.0;
-        double wy = lane < nw ? s_wy[lane] : 0.0;
-#pragma unroll
-        for (int d = 1; d < 32; d <<= 1) {
-          wx = __dadd_rn(wx, __shfl_xor_sync(0xffffffffu, wx, d));
-          wy = __dadd_rn(wy, __shfl_xor_sync(0xffffffffu, wy, d));
-        }
-        if (lane == 0) {
-          s_round[rr] = wx;
-          s_round[32 + rr] = wy;
-        }
-      }
-      __syncthreads();
+      rmx[rr] = sx;  // this warp's subtree of round rr
+      rmy[rr] = sy;
     }
   }
-  const wq_t S = carry;
+  // warp inclusive scans of the thread totals, per round (exact integers)
+  wq_t wexcl[R];
+#pragma unroll
+  for (int rr = 0; rr < R; ++rr) {
+    wq_t x = thr_tot[rr];
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const wq_t y = __shfl_up_sync(0xffffffffu, x, d);
+      if (lane >= d) x += y;
+    }
+    wexcl[rr] = x - thr_tot[rr];
+    if (lane == 31) s_wtot[rr * NW + wid] = (long long)x;
+  }
+  if constexpr (MODE == M_FP16) {
+#pragma unroll
+    for (int d = 16; d >= 1; d >>= 1) {
+      mx_i += __shfl_xor_sync(0xffffffffu, mx_i, d);
+      my_i += __shfl_xor_sync(0xffffffffu, my_i, d);
+    }
+    if (lane == 0) {
+      reinterpret_cast<long long*>(s_misc)[64 + wid] = mx_i;
+      reinterpret_cast<long long*>(s_misc)[96 + wid] = my_i;
+    }
+  } else {
+    if (lane == 0) {
+#pragma unroll
+      for (int rr = 0; rr < R; ++rr) {
+        s_misc[64 + rr * NW + wid] = rmx[rr];
+        s_misc[96 + rr * NW + wid] = rmy[rr];
+      }
+    }
+  }
+  __syncthreads();
+  // prefix of this thread's segment = all earlier (round, warp) totals
+  wq_t S = 0, before = 0;
+  wq_t pre[R];
+#pragma unroll
+  for (int rr = 0; rr < R; ++rr) {
+#pragma unroll
+    for (int w = 0; w < NW; ++w) {
+      const wq_t t = (wq_t)s_wtot[rr * NW + w];
+      if (w == wid) pre[rr] = before;
+      before += t;
+    }
+  }
+  S = before;
   // local cdf c_j = d(cum_j / S), forced to 1 where cum_j == S
-  auto cdf_of = [&](wq_t cum) -> real {
+  auto cdf_of = [&](wq_t cm) -> real {
     if constexpr (MODE == M_FP16) {
       const float invf = __fdiv_rn(1.0f, (float)S);
-      return (cum == S) ? __float2half(1.0f) : __float2half_rn(__fmul_rn((float)cum, invf));
+      return (cm == S) ? __float2half(1.0f) : __float2half_rn(__fmul_rn((float)cm, invf));
     } else {
       const double inv = __ddiv_rn(1.0, (double)S);
-      const double cd = __dmul_rn((double)cum, inv);
+      const double cd = __dmul_rn((double)cm, inv);
       if constexpr (MODE == M_FP32)
-        return (cum == S) ? 1.0f : __double2float_rn(cd);
+        return (cm == S) ? 1.0f : __double2float_rn(cd);
       else
-        return (cum == S) ? 1.0 : cd;
+        return (cm == S) ? 1.0 : cd;
     }
   };
-  if (R == 1) {
-    const int l0 = tid * VPT;
+#pragma unroll
+  for (int rr = 0; rr < R; ++rr) {
+    const int l0 = (rr * TPB + tid) * VPT;
     real cv[VPT];
 #pragma unroll
-    for (int i = 0; i < VPT; ++i) cv[i] = cdf_of(cum_r[i]);
+    for (int i = 0; i < VPT; ++i) cv[i] = cdf_of(pre[rr] + wexcl[rr] + cum[rr][i]);
     constexpr int VB = VPT * (int)sizeof(real);
-    if (l0 + VPT <= Tb && (VB == 4 || VB == 8 || VB == 16) &&
-        ((((size_t)track * K + base + l0) * sizeof(real)) % VB) == 0) {
+    if (l0 + VPT <= Tb && (VB == 4 || VB == 8 || VB == 16) && ((((size_t)track * K) * sizeof(real)) % VB) == 0) {
       if constexpr (VB == 16) {
         uint4 o;
         memcpy(&o, cv, 16);
@@ -1001,44 +1009,34 @@ __global__ void __launch_bounds__(PF_TILE / VPT) pf_fused_frame(FusedArgs a) {
       for (int i = 0; i < VPT; ++i)
         if (l0 + i < Tb) Cn[base + l0 + i] = cv[i];
     }
-  } else {
-    __syncthreads();
-    for (int l = tid; l < Tb; l += TPB) Cn[base + l] = cdf_of(reinterpret_cast<const wq_t*>(s_X)[l]);
   }
-  const size_t ri = (size_t)track * n + tile;
-  if constexpr (MODE == M_FP16) {
-#pragma unroll
-    for (int d = 16; d >= 1; d >>= 1) {
-      mx_i += __shfl_xor_sync(0xffffffffu, mx_i, d);
-      my_i += __shfl_xor_sync(0xffffffffu, my_i, d);
-    }
-    if (lane == 0) {
-      s_red[wid] = mx_i;
-      s_red[32 + wid] = my_i;
-    }
-    __syncthreads();
-    if (tid == 0) {
+  // tile record
+  if (tid == 0) {
+    const size_t ri = (size_t)track * n + tile;
+    a.rec_m[ri] = to_d(mtile);
+    a.rec_S[ri] = (long long)S;
+    if constexpr (MODE == M_FP16) {
       long long sx = 0, sy = 0;
-      for (int w = 0; w < nw; ++w) {
-        sx += s_red[w];
-        sy += s_red[32 + w];
+      for (int w = 0; w < NW; ++w) {
+        sx += reinterpret_cast<long long*>(s_misc)[64 + w];
+        sy += reinterpret_cast<long long*>(s_misc)[96 + w];
       }
-      a.rec_m[ri] = mtile_d;
-      a.rec_S[ri] = (long long)S;
       a.rec_X[ri] = sx;
       a.rec_Y[ri] = sy;
-    }
-  } else {
-    if (tid == 0) {
-      for (int width = R; width > 1; width >>= 1)
-        for (int w = 0; w < width / 2; ++w) {
-          s_round[w] = __dadd_rn(s_round[2 * w], s_round[2 * w + 1]);
-          s_round[32 + w] = __dadd_rn(s_round[32 + 2 * w], s_round[32 + 2 * w + 1]);
+    } else {
+      // canonical tree over the (round, warp) subtrees: contiguous aligned blocks
+      double bx[R * NW], by[R * NW];
+      for (int e = 0; e < R * NW; ++e) {
+        bx[e] = s_misc[64 + e];
+        by[e] = s_misc[96 + e];
+      }
+      for (int width = R * NW; width > 1; width >>= 1)
+        for (int e = 0; e < width / 2; ++e) {
+          bx[e] = __dadd_rn(bx[2 * e], bx[2 * e + 1]);
+          by[e] = __dadd_rn(by[2 * e], by[2 * e + 1]);
         }
-      a.rec_m[ri] = mtile_d;
-      a.rec_S[ri] = (long long)S;
-      a.rec_X[ri] = __double_as_longlong(s_round[0]);
-      a.rec_Y[ri] = __double_as_longlong(s_round[32]);
+      a.rec_X[ri] = __double_as_longlong(bx[0]);
+      a.rec_Y[ri] = __double_as_longlong(by[0]);
     }
   }
 }
@@ -1060,8 +1058,7 @@ struct TableArgs {
   double* tab_O;
   double* tab_invM;
   double* u_out;
-  unsigned long long* s_frame;  // out: per-track stream state at position (t+1)(2K+1)
-  unsigned long long f2k_a, f2k_c;  // f^(2K)
+  unsigned long long ua, uc;  // f^(t(2K+1)+2K): uniform word = ua * x0[track] + uc
   double* traj;       // [track][F][2]
   int traj_stride;    // frames per track in traj
   int traj_index;     // frame slot
@@ -1105,14 +1102,11 @@ __global__ void __launch_bounds__(1024) pf_tile_table(TableArgs a) {
   const long long* rX = a.rec_X + (size_t)track * n;
   const long long* rY = a.rec_Y + (size_t)track * n;
 
-  // the frame's resampling uniform: stream position t(2K+1)+2K = f^(2K) of
-  // the frame base state; one more step is the next frame's base state
-  if (tid == 0) {
-    const unsigned long long st = a.t == 0 ? a.x0[track] : a.s_frame[track];
-    const unsigned long long wu = pfr::apply(pfr::Affine{a.f2k_a, a.f2k_c}, st);
-    s_d[97] = pfr::uniform_of(wu);
-    a.s_frame[track] = pfr::kA * wu + pfr::kC;
-  }
+  pdl_launch_dependents();
+  // the frame's resampling uniform: stream position t(2K+1)+2K, an affine
+  // jump of the seed state passed as an argument
+  if (tid == 0) s_d[97] = pfr::uniform_of(a.ua * a.x0[track] + a.uc);
+  pdl_wait();  // tile records of this frame's fused kernel
   // 1. global max (exact)
   double m = __longlong_as_double(0xfff0000000000000LL);
   double m1 = m;
