@@ -234,7 +234,7 @@ def run_reference_arm(args, cfg, rank, world):
 def _config_block(cfg, args):
     return {"workload": cfg["desc"], "width": cfg["W"], "height": cfg["H"], "frames": cfg["F"],
             "particles_per_track": cfg["K"], "tracks": cfg["tracks"], "precision": cfg["precision"],
-            "tpb": args.tpb, "l2": "flushed (512 MiB write) before every timed step",
+            "tpb": args.tpb or ("128 (fp16) / 256 (fp32, fp64) library defaults"), "l2": "flushed (512 MiB write) before every timed step",
             "rng": "counter-based LCG (device)", "parallelism": f"tracks/GPU, {args.gpus} GPU(s), no collective"}
 
 
@@ -250,7 +250,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
     ap.add_argument("--precision", default=None)
-    ap.add_argument("--tpb", type=int, default=256)
+    ap.add_argument("--tpb", type=int, default=0, help="threads per block (0 = library default per precision)")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-extra", action="store_true", help="skip the FP32/FP64 side measurements")

@@ -292,7 +292,7 @@ static int validate(const pf_config* c, std::string& err) {
     err = "bad shape / template / seeds";
     return PF_EINVAL;
   }
-  int tpb = c->tpb ? c->tpb : 256;
+  int tpb = c->tpb ? c->tpb : 128;
   if (tpb != 32 && tpb != 64 && tpb != 128 && tpb != 256 && tpb != 512 && tpb != 1024) {
     err = "tpb must be a power of two in [32, 1024]";
     return PF_EINVAL;
@@ -313,7 +313,8 @@ int pf_create(pf_handle** out, const pf_config* cfg) {
   h->H = cfg->height;
   h->n_tracks = cfg->n_tracks;
   h->n_videos = cfg->n_videos;
-  h->tpb = cfg->tpb ? cfg->tpb : 256;
+  // default threads per block per precision (measured, bench TPB sweep)
+  h->tpb = cfg->tpb ? cfg->tpb : (cfg->precision >= PF_FP16 ? 128 : 256);
   h->vpt = h->tpb >= 1024 ? 1 : h->tpb >= 512 ? 2 : h->tpb >= 256 ? 4 : 8;
   h->params = cfg->params;
   h->n_off = cfg->n_offsets;

@@ -547,8 +547,8 @@ __device__ __forceinline__ typename Tr<MODE>::vec prop(typename Tr<MODE>::vec xa
 }
 
 template <int MODE>
-constexpr int max_src_tiles() {
-  return MODE == M_FP64 ? 2 : (MODE == M_FP32 ? 4 : 6);
+constexpr int max_src_tiles() {  // speculatively staged source tiles around the CTA's own
+  return MODE == M_FP64 ? 3 : (MODE == M_FP32 ? 4 : 6);
 }
 
 constexpr int kSlowQ = 128;  // deferred ziggurat slow paths per CTA (overflow -> inline)
@@ -706,79 +706,87 @@ __global__ void __launch_bounds__(PF_TILE / (VPT * R)) pf_fused_frame(FusedArgs 
     }
   }
   __syncthreads();
-  {
+  // ---- warp 0: wait for the previous kernels, find the source window;
+  //      other warps: resolve queued slow paths, wait, and speculatively
+  //      stage the local CDFs of the MS tiles around this one (verified
+  //      against the window below; global search otherwise) -------------
+  const int spec_lo = max(0, min(tile - (MS - 1) / 2, n - MS));
+  const int spec_hi = min(n - 1, spec_lo + MS - 1);
+  if (wid == 0 || NW == 1) {
+    pdl_wait();
+    if (a.t > 0) {
+      const int kf = base, kl = base + Tb - 1;
+      const int w0 = max(0, min(tile - 16, n - 32));
+      const int bw = min(w0 + lane, n - 1);
+      const int sv = (int)__ldg(ts + bw);
+      int res[2];
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int kk = e == 0 ? kf : kl;
+        const unsigned ball = __ballot_sync(0xffffffffu, sv <= kk);
+        const int topb = min(w0 + 31, n - 1);
+        int b = -1;
+        if (ball != 0 && (ball != 0xffffffffu || topb == n - 1)) b = min(w0 + 31 - __clz(ball), n - 1);
+        if (b < 0) {
+          int lo = 0, hi = n - 1;
+          while (lo < hi) {
+            const int mid = (lo + hi + 1) >> 1;
+            if ((int)__ldg(ts + mid) <= kk)
+              lo = mid;
+            else
+              hi = mid - 1;
+          }
+          b = lo;
+        }
+        res[e] = b;
+      }
+      const int nsrc = res[1] - res[0] + 1;
+      const int staged = (res[0] >= spec_lo && res[1] <= spec_hi) ? 1 : 0;
+      if (lane == 0) {
+        s_int[0] = res[0];
+        s_int[1] = res[1];
+        s_int[2] = staged;
+      }
+      if (staged && lane <= nsrc) {
+        const int b = min(res[0] + lane, n - 1);
+        s_ts[lane] = lane < nsrc ? (int)__ldg(ts + b) : K;
+        s_tO[lane] = __ldg(tO + b);
+        s_tM[lane] = __ldg(tM + b);
+      }
+    }
+  }
+  if (wid > 0 || NW == 1) {
+    const int t0 = NW == 1 ? tid : tid - 32, nt = NW == 1 ? TPB : TPB - 32;
     const int nq = min(s_int[3], kSlowQ);
-    for (int e = tid; e < nq; e += TPB) {
+    for (int e = t0; e < nq; e += nt) {
       const int sl = s_qs[e];
       set_comp<MODE>(s_X[sl >> 1], sl & 1, pfr::zig_slow(s_qw[e]));
     }
-  }
-  // ---- everything below consumes the previous kernels' results ----------
-  pdl_wait();
-  const double u = a.t > 0 ? a.u_prev[track] : 0.0;
-  if (a.t > 0 && wid == 0) {  // source window: last tile with s_b <= first / last output
-    const int kf = base, kl = base + Tb - 1;
-    const int w0 = max(0, min(tile - 16, n - 32));
-    const int bw = min(w0 + lane, n - 1);
-    const int sv = (int)__ldg(ts + bw);
-    int res[2];
-#pragma unroll
-    for (int e = 0; e < 2; ++e) {
-      const int kk = e == 0 ? kf : kl;
-      const unsigned ball = __ballot_sync(0xffffffffu, sv <= kk);
-      const int topb = min(w0 + 31, n - 1);
-      int b = -1;
-      if (ball != 0 && (ball != 0xffffffffu || topb == n - 1)) b = min(w0 + 31 - __clz(ball), n - 1);
-      if (b < 0) {
-        int lo = 0, hi = n - 1;
-        while (lo < hi) {
-          const int mid = (lo + hi + 1) >> 1;
-          if ((int)__ldg(ts + mid) <= kk)
-            lo = mid;
-          else
-            hi = mid - 1;
-        }
-        b = lo;
-      }
-      res[e] = b;
-    }
-    const int nsrc = res[1] - res[0] + 1;
-    const int staged = nsrc <= MS ? 1 : 0;
-    if (lane == 0) {
-      s_int[0] = res[0];
-      s_int[1] = res[1];
-      s_int[2] = staged;
-    }
-    if (staged && lane <= nsrc) {
-      const int b = min(res[0] + lane, n - 1);
-      s_ts[lane] = lane < nsrc ? (int)__ldg(ts + b) : K;
-      s_tO[lane] = __ldg(tO + b);
-      s_tM[lane] = __ldg(tM + b);
-    }
-  }
-  __syncthreads();  // window + slow-path noise visible
-  int b_lo = 0, b_hi = 0, staged = 0;
-  if (a.t > 0) {
-    b_lo = s_int[0];
-    b_hi = s_int[1];
-    staged = s_int[2];
-    if (staged) {  // 16-byte copies of the source tiles' local CDFs
-      const int c0 = b_lo * PF_TILE;
-      const int cnt = min((b_hi + 1) * PF_TILE, K) - c0;
+    if (NW > 1) pdl_wait();
+    if (a.t > 0) {  // speculative 16-byte staging of tiles spec_lo .. spec_hi
+      const int c0 = spec_lo * PF_TILE;
+      const int cnt = min((spec_hi + 1) * PF_TILE, K) - c0;
       constexpr int PER = 16 / sizeof(real);
       if ((((size_t)track * K) % PER) == 0) {
         const int nvec = cnt / PER;
         const uint4* src = reinterpret_cast<const uint4*>(Cp + c0);
         uint4* dst = reinterpret_cast<uint4*>(s_c);
-        for (int i = tid; i < nvec; i += TPB) dst[i] = __ldg(src + i);
-        for (int i = nvec * PER + tid; i < cnt; i += TPB) s_c[i] = Cp[c0 + i];
+        for (int i = t0; i < nvec; i += nt) dst[i] = __ldg(src + i);
+        for (int i = nvec * PER + t0; i < cnt; i += nt) s_c[i] = Cp[c0 + i];
       } else {
-        for (int i = tid; i < cnt; i += TPB) s_c[i] = Cp[c0 + i];
+        for (int i = t0; i < cnt; i += nt) s_c[i] = Cp[c0 + i];
       }
-      __syncthreads();
     }
   }
-  const real* Csrc = staged ? s_c - b_lo * PF_TILE : Cp;
+  const double u = a.t > 0 ? a.u_prev[track] : 0.0;
+  __syncthreads();  // window, slow-path noise and staged CDFs visible
+  int b_lo = 0, b_hi = 0, staged = 0;
+  if (a.t > 0) {
+    b_lo = s_int[0];
+    b_hi = s_int[1];
+    staged = s_int[2];
+  }
+  const real* Csrc = staged ? s_c - spec_lo * PF_TILE : Cp;
   const double invK = __ddiv_rn(1.0, (double)K);
 
   vec drift, stdv;
