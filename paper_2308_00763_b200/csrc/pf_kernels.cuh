@@ -547,7 +547,7 @@ __device__ __forceinline__ typename Tr<MODE>::vec prop(typename Tr<MODE>::vec xa
 }
 
 template <int MODE>
-constexpr int max_src_tiles() {  // speculatively staged source tiles around the CTA's own
+constexpr int max_src_tiles() {  // source tiles staged in shared memory (else global search)
   return MODE == M_FP64 ? 3 : (MODE == M_FP32 ? 4 : 6);
 }
 
@@ -688,11 +688,16 @@ __global__ void __launch_bounds__(PF_TILE / (VPT * R)) pf_fused_frame(FusedArgs 
       for (int c = 0; c < 2; ++c) {
         const unsigned long long w = xs;
         xs = pfr::kA * xs + pfr::kC;
-        const unsigned idx = (unsigned)(w >> 56);
-        const unsigned long long rabs = (w >> 3) & pfr::kMask52;
-        const double x = __dmul_rn((double)rabs, s_wi[idx]);
-        nn[c] = ((w >> 55) & 1) ? -x : x;
-        if ((unsigned)(rabs >> 20) >= s_kihi[idx] && l0 + i < Tb) {
+        const unsigned whi = (unsigned)(w >> 32), wlo = (unsigned)w;
+        const unsigned idx = whi >> 24;
+        // rabs = bits 3..54 of w; (double)rabs exactly via the 2^52 bias trick
+        const unsigned rlo = __funnelshift_r(wlo, whi, 3);
+        const unsigned rhi = (whi >> 3) & 0xfffffu;
+        const double rabs_d = __dsub_rn(__hiloint2double(0x43300000 | rhi, rlo), 4503599627370496.0);
+        const double x = __dmul_rn(rabs_d, s_wi[idx]);
+        // sign (bit 55) flips the sign bit of the product
+        nn[c] = __hiloint2double(__double2hiint(x) ^ ((whi << 8) & 0x80000000u), __double2loint(x));
+        if (((rhi << 12) | (rlo >> 20)) >= s_kihi[idx] && l0 + i < Tb) {
           const int slot = atomicAdd(&s_int[3], 1);
           if (slot < kSlowQ) {
             s_qw[slot] = w;
@@ -706,12 +711,9 @@ __global__ void __launch_bounds__(PF_TILE / (VPT * R)) pf_fused_frame(FusedArgs 
     }
   }
   __syncthreads();
-  // ---- warp 0: wait for the previous kernels, find the source window;
-  //      other warps: resolve queued slow paths, wait, and speculatively
-  //      stage the local CDFs of the MS tiles around this one (verified
-  //      against the window below; global search otherwise) -------------
-  const int spec_lo = max(0, min(tile - (MS - 1) / 2, n - MS));
-  const int spec_hi = min(n - 1, spec_lo + MS - 1);
+  // ---- warp 0: wait for the previous kernels and find the source window
+  //      (tiles whose outputs cover this tile); other warps meanwhile resolve
+  //      the queued slow paths ---------------------------------------------
   if (wid == 0 || NW == 1) {
     pdl_wait();
     if (a.t > 0) {
@@ -741,7 +743,7 @@ __global__ void __launch_bounds__(PF_TILE / (VPT * R)) pf_fused_frame(FusedArgs 
         res[e] = b;
       }
       const int nsrc = res[1] - res[0] + 1;
-      const int staged = (res[0] >= spec_lo && res[1] <= spec_hi) ? 1 : 0;
+      const int staged = nsrc <= MS ? 1 : 0;
       if (lane == 0) {
         s_int[0] = res[0];
         s_int[1] = res[1];
@@ -763,30 +765,31 @@ __global__ void __launch_bounds__(PF_TILE / (VPT * R)) pf_fused_frame(FusedArgs 
       set_comp<MODE>(s_X[sl >> 1], sl & 1, pfr::zig_slow(s_qw[e]));
     }
     if (NW > 1) pdl_wait();
-    if (a.t > 0) {  // speculative 16-byte staging of tiles spec_lo .. spec_hi
-      const int c0 = spec_lo * PF_TILE;
-      const int cnt = min((spec_hi + 1) * PF_TILE, K) - c0;
-      constexpr int PER = 16 / sizeof(real);
-      if ((((size_t)track * K) % PER) == 0) {
-        const int nvec = cnt / PER;
-        const uint4* src = reinterpret_cast<const uint4*>(Cp + c0);
-        uint4* dst = reinterpret_cast<uint4*>(s_c);
-        for (int i = t0; i < nvec; i += nt) dst[i] = __ldg(src + i);
-        for (int i = nvec * PER + t0; i < cnt; i += nt) s_c[i] = Cp[c0 + i];
-      } else {
-        for (int i = t0; i < cnt; i += nt) s_c[i] = Cp[c0 + i];
-      }
-    }
   }
   const double u = a.t > 0 ? a.u_prev[track] : 0.0;
-  __syncthreads();  // window, slow-path noise and staged CDFs visible
+  __syncthreads();  // window and slow-path noise visible
   int b_lo = 0, b_hi = 0, staged = 0;
   if (a.t > 0) {
     b_lo = s_int[0];
     b_hi = s_int[1];
     staged = s_int[2];
+    if (staged) {  // 16-byte copies of exactly the source tiles' local CDFs
+      const int c0 = b_lo * PF_TILE;
+      const int cnt = min((b_hi + 1) * PF_TILE, K) - c0;
+      constexpr int PER = 16 / sizeof(real);
+      if ((((size_t)track * K) % PER) == 0) {
+        const int nvec = cnt / PER;
+        const uint4* src = reinterpret_cast<const uint4*>(Cp + c0);
+        uint4* dst = reinterpret_cast<uint4*>(s_c);
+        for (int i = tid; i < nvec; i += TPB) dst[i] = __ldg(src + i);
+        for (int i = nvec * PER + tid; i < cnt; i += TPB) s_c[i] = Cp[c0 + i];
+      } else {
+        for (int i = tid; i < cnt; i += TPB) s_c[i] = Cp[c0 + i];
+      }
+      __syncthreads();
+    }
   }
-  const real* Csrc = staged ? s_c - spec_lo * PF_TILE : Cp;
+  const real* Csrc = staged ? s_c - b_lo * PF_TILE : Cp;
   const double invK = __ddiv_rn(1.0, (double)K);
 
   vec drift, stdv;
@@ -827,7 +830,12 @@ __global__ void __launch_bounds__(PF_TILE / (VPT * R)) pf_fused_frame(FusedArgs 
         }
         b = lo;
       }
-      int jprev = 0, bprev = -1;
+      // register-cached geometry of the current source tile
+      int sb = tab_s(b), snext = b < b_hi ? tab_s(b + 1) : K;
+      double gO = tab_O(b), gM = tab_M(b);
+      int tl = b * PF_TILE, tb = min(PF_TILE, K - tl);
+      const real* cb = Csrc + tl;
+      int jprev = -1;
 #pragma unroll
       for (int i = 0; i < VPT; ++i) {
         const int k = base + l0 + i;
@@ -835,27 +843,39 @@ __global__ void __launch_bounds__(PF_TILE / (VPT * R)) pf_fused_frame(FusedArgs 
           anc[i] = k;
           continue;
         }
-        while (b < b_hi && tab_s(b + 1) <= k) ++b;
+        if (k >= snext) {  // next source tile (rare: outputs of one source tile are contiguous)
+          do {
+            ++b;
+            snext = b < b_hi ? tab_s(b + 1) : K;
+          } while (k >= snext);
+          sb = tab_s(b);
+          gO = tab_O(b);
+          gM = tab_M(b);
+          tl = b * PF_TILE;
+          tb = min(PF_TILE, K - tl);
+          cb = Csrc + tl;
+          jprev = -1;
+        }
         typename KT::k_t kq;
         if constexpr (MODE == M_FP16) {
           // f32 tile-local point: q = ((k - s_b) + phi_b) * rho_b
-          const float qf = __fmul_rn(__fadd_rn((float)(k - tab_s(b)), (float)tab_O(b)), (float)tab_M(b));
+          const float qf = __fmul_rn(__fadd_rn((float)(k - sb), (float)gO), (float)gM);
           kq = __half_as_ushort(__float2half_ru(fminf(fmaxf(qf, 0.0f), 1.0f)));
         } else {
           const double p = point_of<MODE>(k, u, K, invK);
-          const double im = tab_M(b);
-          const double q = im == 0.0 ? 0.0 : __dmul_rn(__dsub_rn(p, tab_O(b)), im);
+          const double q = gM == 0.0 ? 0.0 : __dmul_rn(__dsub_rn(p, gO), gM);
           kq = KT::up(fmin(fmax(q, 0.0), 1.0));
         }
-        const int tl = b * PF_TILE;
-        const int tb = min(PF_TILE, K - tl);
-        const real* cb = Csrc + tl;
-        int j = (b == bprev) ? advance_key<MODE>(cb, jprev, tb, kq) : lb_branchless<MODE>(cb, tb, kq);
+        int j = jprev >= 0 ? advance_key<MODE>(cb, jprev, tb, kq) : lb_branchless<MODE>(cb, tb, kq);
         j = min(j, tb - 1);
         jprev = j;
-        bprev = b;
         anc[i] = tl + j;
       }
+    }
+    if (a.dbg_anc != nullptr) {
+#pragma unroll
+      for (int i = 0; i < VPT; ++i)
+        if (l0 + i < Tb) a.dbg_anc[(size_t)track * K + base + l0 + i] = anc[i];
     }
 #pragma unroll
     for (int i = 0; i < VPT; ++i) {
@@ -869,13 +889,20 @@ __global__ void __launch_bounds__(PF_TILE / (VPT * R)) pf_fused_frame(FusedArgs 
         Lr[rr][i] = L;
         Xr[rr][i] = xn;
         if (gt_real<MODE>(L, tmax)) tmax = L;
-        if (a.dbg_anc) a.dbg_anc[(size_t)track * K + base + l] = anc[i];
-        if (a.dbg_L) reinterpret_cast<real*>(a.dbg_L)[(size_t)track * K + base + l] = L;
       } else {
         Lr[rr][i] = neg_inf<MODE>();
         Xr[rr][i].x = (real)0;
         Xr[rr][i].y = (real)0;
       }
+    }
+  }
+  if (a.dbg_anc != nullptr) {  // debug capture (parity tests): recompute-free copies
+#pragma unroll
+    for (int rr = 0; rr < R; ++rr) {
+      const int l0 = (rr * TPB + tid) * VPT;
+#pragma unroll
+      for (int i = 0; i < VPT; ++i)
+        if (l0 + i < Tb) reinterpret_cast<real*>(a.dbg_L)[(size_t)track * K + base + l0 + i] = Lr[rr][i];
     }
   }
   // tile max (exact): warp max, one barrier, every thread reduces the NW values
@@ -978,12 +1005,12 @@ __global__ void __launch_bounds__(PF_TILE / (VPT * R)) pf_fused_frame(FusedArgs 
   }
   S = before;
   // local cdf c_j = d(cum_j / S), forced to 1 where cum_j == S
+  const float invf = MODE == M_FP16 ? __fdiv_rn(1.0f, (float)S) : 0.0f;
+  const double inv = MODE == M_FP16 ? 0.0 : __ddiv_rn(1.0, (double)S);
   auto cdf_of = [&](wq_t cm) -> real {
     if constexpr (MODE == M_FP16) {
-      const float invf = __fdiv_rn(1.0f, (float)S);
       return (cm == S) ? __float2half(1.0f) : __float2half_rn(__fmul_rn((float)cm, invf));
     } else {
-      const double inv = __ddiv_rn(1.0, (double)S);
       const double cd = __dmul_rn((double)cm, inv);
       if constexpr (MODE == M_FP32)
         return (cm == S) ? 1.0f : __double2float_rn(cd);
