@@ -142,7 +142,10 @@ struct pf_handle {
   double start_x = 0, start_y = 0;
   int device = 0;
   cudaStream_t stream = nullptr;
-  int n_tiles = 0, n_pad = 1, Q = 52, tpb_table = 32;
+  int n_tiles = 0, n_pad = 1, Q = 52, tpb_table = 32, n_chunks = 1;
+  unsigned long long* tsync = nullptr;
+  long long* tagg = nullptr;
+  double* troots = nullptr;
   size_t rs = 8, vs = 16;
   void* X[2] = {nullptr, nullptr};
   void* C[2] = {nullptr, nullptr};
@@ -253,7 +256,7 @@ int pf_destroy(pf_handle* h) {
   if (!h) return PF_OK;
   cudaSetDevice(h->device);
   void* ptrs[] = {h->X[0], h->X[1], h->C[0], h->C[1], h->rec_m, h->rec_S, h->rec_X, h->rec_Y, h->tab_s, h->tab_O,
-                  h->tab_invM, h->u, h->x0, h->tj, h->tt, h->exp16, h->zig, h->d_offs, h->d_plan, h->d_leaves, h->d_frames,
+                  h->tab_invM, h->u, h->x0, h->tj, h->tt, h->tsync, h->tagg, h->troots, h->exp16, h->zig, h->d_offs, h->d_plan, h->d_leaves, h->d_frames,
                   h->d_maps, h->d_traj, h->d_degen, h->dbg_anc, h->dbg_L};
   for (void* p : ptrs)
     if (p) cudaFree(p);
@@ -334,7 +337,9 @@ int pf_create(pf_handle** out, const pf_config* cfg) {
   int lg = 0;
   while ((1LL << lg) < h->n_tiles) ++lg;
   h->Q = 52 - lg;
-  h->tpb_table = std::min(1024, std::max(32, h->n_pad));
+  // tile table: one tile per thread; chunks of 128 tiles per CTA when n > 128
+  h->tpb_table = h->n_pad <= 128 ? std::max(32, h->n_pad) : 128;
+  h->n_chunks = (h->n_tiles + h->tpb_table - 1) / h->tpb_table;
   std::string& e = h->err;
 #define CK(x)                    \
   do {                           \
@@ -371,6 +376,10 @@ int pf_create(pf_handle** out, const pf_config* cfg) {
   CK(cudack(cudaMalloc(&h->tab_invM, NT * 8), "tab"));
   CK(cudack(cudaMalloc(&h->u, h->n_tracks * 8), "u"));
   CK(cudack(cudaMalloc(&h->d_degen, h->n_tracks * sizeof(int)), "degen"));
+  CK(cudack(cudaMalloc(&h->tsync, (size_t)h->n_tracks * 4 * 8), "tsync"));
+  CK(cudack(cudaMemset(h->tsync, 0, (size_t)h->n_tracks * 4 * 8), "tsync"));
+  CK(cudack(cudaMalloc(&h->tagg, (size_t)h->n_tracks * h->n_chunks * 8), "tagg"));
+  CK(cudack(cudaMalloc(&h->troots, (size_t)h->n_tracks * h->n_chunks * 3 * 8), "troots"));
   // per-track LCG seed states
   std::vector<unsigned long long> x0(h->n_tracks);
   for (int i = 0; i < h->n_tracks; ++i) x0[i] = pfr::seed_state(cfg->seeds[i]);
@@ -474,6 +483,7 @@ int pf_reset(pf_handle* h, double x0, double y0) {
   std::vector<int> dg(h->n_tracks, INT_MAX);
   PF_CUDA(cudaMemcpyAsync(h->d_degen, dg.data(), h->n_tracks * sizeof(int), cudaMemcpyHostToDevice, h->stream),
           h->err);
+  PF_CUDA(cudaMemsetAsync(h->tsync, 0, (size_t)h->n_tracks * 4 * 8, h->stream), h->err);
   PF_CUDA(cudaStreamSynchronize(h->stream), h->err);
   return PF_OK;
 }
@@ -582,7 +592,11 @@ static int launch_frame(pf_handle* h, const void* map_slot, long long map_video_
   t.degenerate = h->d_degen;
   const void* tk = h->km == 0 ? (const void*)pfk::pf_tile_table<0>
                    : h->km == 1 ? (const void*)pfk::pf_tile_table<1> : (const void*)pfk::pf_tile_table<2>;
-  PF_CUDA(launch_pdl(h, tk, dim3(h->n_tracks), dim3(h->tpb_table), 0, t), h->err);
+  t.n_chunks = h->n_chunks;
+  t.sync = h->tsync;
+  t.agg = h->tagg;
+  t.roots = h->troots;
+  PF_CUDA(launch_pdl(h, tk, dim3(h->n_chunks, h->n_tracks), dim3(h->tpb_table), 0, t), h->err);
   PF_CUDA(cudaGetLastError(), h->err);
   if (h->profiling) PF_CUDA(cudaEventRecord(h->pev[3 * traj_index + 2], h->stream), h->err);
   h->launches += 2;

@@ -548,16 +548,18 @@ __device__ __forceinline__ typename Tr<MODE>::vec prop(typename Tr<MODE>::vec xa
 
 template <int MODE>
 constexpr int max_src_tiles() {  // source tiles staged in shared memory (else global search)
-  return MODE == M_FP64 ? 3 : (MODE == M_FP32 ? 4 : 6);
+  return MODE == M_FP64 ? 3 : 4;
 }
 
 constexpr int kSlowQ = 128;  // deferred ziggurat slow paths per CTA (overflow -> inline)
 
+// shared-memory footprint: ziggurat tables, noise/positions (vec per particle),
+// staged source CDFs, table slice, slow-path queue, reduction scratch
 template <int MODE>
 constexpr size_t fused_smem_bytes() {
   using real = typename Tr<MODE>::real;
   using vec = typename Tr<MODE>::vec;
-  return 3072 + PF_TILE * (sizeof(real) + sizeof(vec)) + max_src_tiles<MODE>() * PF_TILE * sizeof(real) +
+  return 3072 + PF_TILE * sizeof(vec) + max_src_tiles<MODE>() * PF_TILE * sizeof(real) +
          (max_src_tiles<MODE>() + 1) * 24 + kSlowQ * 12 + 320 * 8;
 }
 
@@ -629,9 +631,8 @@ __global__ void __launch_bounds__(PF_TILE / (VPT * R)) pf_fused_frame(FusedArgs 
   extern __shared__ __align__(16) unsigned char smem[];
   uint32_t* s_kihi = reinterpret_cast<uint32_t*>(smem);   // 1 KB
   double* s_wi = reinterpret_cast<double*>(smem + 1024);  // 2 KB
-  real* s_L = reinterpret_cast<real*>(smem + 3072);       // R > 1 only
-  vec* s_X = reinterpret_cast<vec*>(smem + 3072 + PF_TILE * sizeof(real));  // noise, then positions (R > 1)
-  real* s_c = reinterpret_cast<real*>(smem + 3072 + PF_TILE * (sizeof(real) + sizeof(vec)));
+  vec* s_X = reinterpret_cast<vec*>(smem + 3072);  // per-particle noise
+  real* s_c = reinterpret_cast<real*>(smem + 3072 + PF_TILE * sizeof(vec));
   unsigned char* p_tab = reinterpret_cast<unsigned char*>(s_c + MS * PF_TILE);
   int* s_ts = reinterpret_cast<int*>(p_tab);                        // MS + 1 (in-track indices)
   double* s_tO = reinterpret_cast<double*>(p_tab + (MS + 1) * 8);   // MS + 1
@@ -1098,6 +1099,10 @@ struct TableArgs {
   int traj_stride;    // frames per track in traj
   int traj_index;     // frame slot
   int* degenerate;    // per track: first degenerate frame (or INT_MAX)
+  int n_chunks;                 // CTAs per track (chunks of blockDim.x tiles)
+  unsigned long long* sync;     // per track: [0] max key, [1] arrivals (max), [2] arrivals (sums), [3] ticket
+  long long* agg;               // per track x chunk: chunk mass total
+  double* roots;                // per track x chunk x 3: estimate subtree roots
 };
 
 // canonical pairwise accumulation over a power-of-two run (binary counter)
@@ -1122,185 +1127,168 @@ struct PwAcc {
   }
 };
 
+// order-preserving map double -> uint64 (for atomicMax); 0 is below every key
+__device__ __forceinline__ unsigned long long okey(double d) {
+  const unsigned long long b = (unsigned long long)__double_as_longlong(d);
+  return (b & 0x8000000000000000ULL) ? ~b : (b | 0x8000000000000000ULL);
+}
+__device__ __forceinline__ double okey_inv(unsigned long long k) {
+  const unsigned long long b = (k & 0x8000000000000000ULL) ? (k & 0x7fffffffffffffffULL) : ~k;
+  return __longlong_as_double((long long)b);
+}
+__device__ __forceinline__ void spin_until(unsigned long long* ctr, unsigned long long target) {
+  while (atomicAdd(ctr, 0ULL) < target) __nanosleep(64);
+}
+
+// Tile table, one CTA per chunk of blockDim.x tiles (one tile per thread),
+// grid (n_chunks, n_tracks).  All cross-CTA combination is exact: the global
+// max is an atomicMax over order-preserving keys, the mass prefix an int64
+// sum of chunk totals, and the estimate a canonical pairwise tree whose
+// chunk subtrees are completed by the last CTA in tree order.  All CTAs of a
+// track are co-resident: each calls launch_dependents on entry, so the next
+// (dependent) grid cannot occupy the GPU before every table CTA has started.
 template <int MODE>
-__global__ void __launch_bounds__(1024) pf_tile_table(TableArgs a) {
+__global__ void __launch_bounds__(128) pf_tile_table(TableArgs a) {
   __shared__ long long s_i[32];
   __shared__ double s_d[3 * 32 + 4];
+  __shared__ int s_last;
   constexpr int FB = Tr<MODE>::FB;
-  const int track = blockIdx.x, tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const int chunk = blockIdx.x, track = blockIdx.y, tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const int TPB = blockDim.x, nw = TPB >> 5;
-  const int n = a.n_tiles;
-  const int Rt = max(1, a.n_pad / TPB);  // tiles per thread (power of two)
-  const int b0 = tid * Rt;
-  const double* rm = a.rec_m + (size_t)track * n;
-  const long long* rS = a.rec_S + (size_t)track * n;
-  const long long* rX = a.rec_X + (size_t)track * n;
-  const long long* rY = a.rec_Y + (size_t)track * n;
+  const int n = a.n_tiles, nc = a.n_chunks;
+  const int b = chunk * TPB + tid;
+  const bool valid = b < n;
+  unsigned long long* sy = a.sync + (size_t)track * 4;
 
   pdl_launch_dependents();
-  // the frame's resampling uniform: stream position t(2K+1)+2K, an affine
-  // jump of the seed state passed as an argument
-  if (tid == 0) s_d[97] = pfr::uniform_of(a.ua * a.x0[track] + a.uc);
+  // the frame's resampling uniform: stream position t(2K+1)+2K
+  const double u = pfr::uniform_of(a.ua * a.x0[track] + a.uc);
   pdl_wait();  // tile records of this frame's fused kernel
+  const size_t rb = (size_t)track * n + (valid ? b : 0);
+  const double m1 = valid ? a.rec_m[rb] : __longlong_as_double(0xfff0000000000000LL);
+  const long long S1 = valid ? a.rec_S[rb] : 0, X1 = valid ? a.rec_X[rb] : 0, Y1 = valid ? a.rec_Y[rb] : 0;
+
   // 1. global max (exact)
-  double m = __longlong_as_double(0xfff0000000000000LL);
-  double m1 = m;
-  long long S1 = 0, X1 = 0, Y1 = 0;
-  if (Rt == 1 && b0 < n) {  // common case: one tile per thread, keep it in registers
-    m1 = rm[b0];
-    S1 = rS[b0];
-    X1 = rX[b0];
-    Y1 = rY[b0];
-    m = m1;
-  } else {
-    for (int i = 0; i < Rt; ++i)
-      if (b0 + i < n) m = fmax(m, rm[b0 + i]);
-  }
+  double m = m1;
 #pragma unroll
   for (int d = 16; d >= 1; d >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, d));
   if (lane == 0) s_d[wid] = m;
   __syncthreads();
-  if (wid == 0) {
-    double mm = lane < nw ? s_d[lane] : s_d[0];
-#pragma unroll
-    for (int d = 16; d >= 1; d >>= 1) mm = fmax(mm, __shfl_xor_sync(0xffffffffu, mm, d));
-    if (lane == 0) s_d[96] = mm;
+  if (tid == 0) {
+    double mm = s_d[0];
+    for (int w = 1; w < nw; ++w) mm = fmax(mm, s_d[w]);
+    if (nc > 1) {
+      atomicMax(sy + 0, okey(mm));
+      __threadfence();
+      atomicAdd(sy + 1, 1ULL);
+      spin_until(sy + 1, (unsigned long long)nc);
+      mm = okey_inv(atomicAdd(sy + 0, 0ULL));
+    }
+    s_d[96] = mm;
   }
   __syncthreads();
   m = s_d[96];
-  const double u = s_d[97];
   const double scale = ldexp(1.0, a.Q - FB);
   const double Kd = __ll2double_rn(a.K);
   const double invK = __ddiv_rn(1.0, Kd);
 
-  auto tile_mass = [&](double mb, long long Sb, double& f) -> long long {
-    f = pfm::exp64(__dsub_rn(mb, m));
-    return __double2ll_rn(__dmul_rn(__dmul_rn((double)Sb, f), scale));
-  };
-  // first output index of tile b: #points <= O (exact for the mode's point formula)
-  auto first_output = [&](double O) -> long long {
-    long long k = (long long)floor(__dsub_rn(__dmul_rn(O, Kd), u));
-    k = min(max(k, 0LL), a.K);
-    while (k > 0 && point_of<MODE>(k - 1, u, a.K, invK) > O) --k;
-    while (k < a.K && point_of<MODE>(k, u, a.K, invK) <= O) ++k;
-    return k;
-  };
+  // 2. exact fixed-point tile mass and its prefix across the chunk / track
+  double f = 0.0;
+  long long mass = 0;
+  if (valid) {
+    f = pfm::exp64(__dsub_rn(m1, m));
+    mass = __double2ll_rn(__dmul_rn(__dmul_rn((double)S1, f), scale));
+  }
+  long long ctot;
+  long long excl = block_excl_scan<long long>(mass, s_i, &ctot);
+  long long Sqi = ctot;
+  if (nc > 1) {
+    long long* ag = a.agg + (size_t)track * nc;
+    if (tid == 0) {
+      ag[chunk] = ctot;
+      __threadfence();
+      atomicAdd(sy + 2, 1ULL);
+      spin_until(sy + 2, (unsigned long long)nc);
+    }
+    __syncthreads();
+    long long before = 0, all = 0;
+    for (int c = tid; c < nc; c += TPB) {
+      const long long v = __ldcg(ag + c);
+      all += v;
+      if (c < chunk) before += v;
+    }
+#pragma unroll
+    for (int d = 16; d >= 1; d >>= 1) {
+      before += __shfl_xor_sync(0xffffffffu, before, d);
+      all += __shfl_xor_sync(0xffffffffu, all, d);
+    }
+    if (lane == 0) {
+      s_i[wid] = before;
+      reinterpret_cast<long long*>(s_d)[wid] = all;
+    }
+    __syncthreads();
+    before = 0;
+    all = 0;
+    for (int w = 0; w < nw; ++w) {
+      before += s_i[w];
+      all += reinterpret_cast<long long*>(s_d)[w];
+    }
+    excl += before;
+    Sqi = all;
+    __syncthreads();
+  }
+  const double Sq = (double)Sqi;
 
-  // resampling geometry of tile b.  FP64/FP32: offset O_b and 1/M_b (the
-  // reference's point formula is evaluated against them).  FP16: the f32
-  // tile-local coordinate q = ((k - s_b) + phi_b) * rho_b with
-  // phi_b = f32(s_b + u - K O_b), rho_b = f32(1 / (K M_b)).
-  auto store_tile_geometry = [&](size_t ti, long long sb, double O, long long mass, double Sq) {
+  // 3. table entries and the estimate moments
+  double vx = 0.0, vy = 0.0, vd = 0.0;
+  if (valid) {
+    const double O = __ddiv_rn((double)excl, Sq);
+    long long sb = 0;
+    if (b > 0) {
+      long long k = (long long)floor(__dsub_rn(__dmul_rn(O, Kd), u));
+      k = min(max(k, 0LL), a.K);
+      while (k > 0 && point_of<MODE>(k - 1, u, a.K, invK) > O) --k;
+      while (k < a.K && point_of<MODE>(k, u, a.K, invK) <= O) ++k;
+      sb = k;
+    }
+    a.tab_s[rb] = sb;
     if constexpr (MODE == M_FP16) {
-      a.tab_O[ti] = (double)__double2float_rn(__dsub_rn(__dadd_rn((double)sb, u), __dmul_rn(Kd, O)));
-      a.tab_invM[ti] = mass > 0 ? (double)__double2float_rn(__ddiv_rn(Sq, __dmul_rn(Kd, (double)mass))) : 0.0;
+      // f32 tile-local coordinate q = ((k - s_b) + phi_b) * rho_b
+      a.tab_O[rb] = (double)__double2float_rn(__dsub_rn(__dadd_rn((double)sb, u), __dmul_rn(Kd, O)));
+      a.tab_invM[rb] = mass > 0 ? (double)__double2float_rn(__ddiv_rn(Sq, __dmul_rn(Kd, (double)mass))) : 0.0;
     } else {
-      a.tab_O[ti] = O;
-      a.tab_invM[ti] = mass > 0 ? __ddiv_rn(Sq, (double)mass) : 0.0;
+      a.tab_O[rb] = O;
+      a.tab_invM[rb] = mass > 0 ? __ddiv_rn(Sq, (double)mass) : 0.0;
     }
-  };
-
-  if (Rt == 1) {
-    const int b = b0;
-    double f = 0.0;
-    const long long mass = b < n ? tile_mass(m1, S1, f) : 0;
-    long long tot;
-    const long long excl = block_excl_scan<long long>(mass, s_i, &tot);
-    const double Sq = (double)tot;
-    double vx = 0.0, vy = 0.0, vd = 0.0;
-    if (b < n) {
-      const double O = __ddiv_rn((double)excl, Sq);
-      const size_t ti = (size_t)track * n + b;
-      const long long sb = b > 0 ? first_output(O) : 0;
-      a.tab_s[ti] = sb;
-      store_tile_geometry(ti, sb, O, mass, Sq);
-      double X, Y;
-      if constexpr (MODE == M_FP16) {
-        X = (double)X1;
-        Y = (double)Y1;
-      } else {
-        X = __longlong_as_double(X1);
-        Y = __longlong_as_double(Y1);
-      }
-      vx = __dmul_rn(f, X);
-      vy = __dmul_rn(f, Y);
-      vd = __dmul_rn(f, (double)S1);
+    double X, Y;
+    if constexpr (MODE == M_FP16) {
+      X = (double)X1;
+      Y = (double)Y1;
+    } else {
+      X = __longlong_as_double(X1);
+      Y = __longlong_as_double(Y1);
     }
-    // canonical pairwise tree: lanes then warps (butterflies, zero padding)
+    vx = __dmul_rn(f, X);
+    vy = __dmul_rn(f, Y);
+    vd = __dmul_rn(f, (double)S1);
+  }
+  // canonical pairwise tree: lanes, warps (zero padded), chunks (last CTA)
 #pragma unroll
-    for (int d = 1; d < 32; d <<= 1) {
-      vx = __dadd_rn(vx, __shfl_xor_sync(0xffffffffu, vx, d));
-      vy = __dadd_rn(vy, __shfl_xor_sync(0xffffffffu, vy, d));
-      vd = __dadd_rn(vd, __shfl_xor_sync(0xffffffffu, vd, d));
-    }
-    if (lane == 0) {
-      s_d[wid] = vx;
-      s_d[32 + wid] = vy;
-      s_d[64 + wid] = vd;
-    }
-  } else {
-    long long loc = 0;
-    for (int i = 0; i < Rt; ++i) {
-      const int b = b0 + i;
-      if (b < n) {
-        double f;
-        loc += tile_mass(rm[b], rS[b], f);
-      }
-    }
-    long long tot;
-    const long long excl = block_excl_scan<long long>(loc, s_i, &tot);
-    const double Sq = (double)tot;
-    long long run = excl;
-    PwAcc ax, ay, ad;
-    ax.reset();
-    ay.reset();
-    ad.reset();
-    for (int i = 0; i < Rt; ++i) {
-      const int b = b0 + i;
-      double vx = 0.0, vy = 0.0, vd = 0.0;
-      if (b < n) {
-        double f;
-        const long long mass = tile_mass(rm[b], rS[b], f);
-        const double O = __ddiv_rn((double)run, Sq);
-        const size_t ti = (size_t)track * n + b;
-        const long long sb = b > 0 ? first_output(O) : 0;
-        a.tab_s[ti] = sb;
-        store_tile_geometry(ti, sb, O, mass, Sq);
-        double X, Y;
-        if constexpr (MODE == M_FP16) {
-          X = (double)rX[b];
-          Y = (double)rY[b];
-        } else {
-          X = __longlong_as_double(rX[b]);
-          Y = __longlong_as_double(rY[b]);
-        }
-        vx = __dmul_rn(f, X);
-        vy = __dmul_rn(f, Y);
-        vd = __dmul_rn(f, (double)rS[b]);
-        run += mass;
-      }
-      ax.push(vx);
-      ay.push(vy);
-      ad.push(vd);
-    }
-    double nx = ax.root(), ny = ay.root(), den = ad.root();
-#pragma unroll
-    for (int d = 1; d < 32; d <<= 1) {
-      nx = __dadd_rn(nx, __shfl_xor_sync(0xffffffffu, nx, d));
-      ny = __dadd_rn(ny, __shfl_xor_sync(0xffffffffu, ny, d));
-      den = __dadd_rn(den, __shfl_xor_sync(0xffffffffu, den, d));
-    }
-    if (lane == 0) {
-      s_d[wid] = nx;
-      s_d[32 + wid] = ny;
-      s_d[64 + wid] = den;
-    }
+  for (int d = 1; d < 32; d <<= 1) {
+    vx = __dadd_rn(vx, __shfl_xor_sync(0xffffffffu, vx, d));
+    vy = __dadd_rn(vy, __shfl_xor_sync(0xffffffffu, vy, d));
+    vd = __dadd_rn(vd, __shfl_xor_sync(0xffffffffu, vd, d));
+  }
+  if (lane == 0) {
+    s_d[wid] = vx;
+    s_d[32 + wid] = vy;
+    s_d[64 + wid] = vd;
   }
   __syncthreads();
   if (wid == 0) {
-    double vx = lane < nw ? s_d[lane] : 0.0;
-    double vy = lane < nw ? s_d[32 + lane] : 0.0;
-    double vd = lane < nw ? s_d[64 + lane] : 0.0;
+    vx = lane < nw ? s_d[lane] : 0.0;
+    vy = lane < nw ? s_d[32 + lane] : 0.0;
+    vd = lane < nw ? s_d[64 + lane] : 0.0;
 #pragma unroll
     for (int d = 1; d < 32; d <<= 1) {
       vx = __dadd_rn(vx, __shfl_xor_sync(0xffffffffu, vx, d));
@@ -1308,17 +1296,85 @@ __global__ void __launch_bounds__(1024) pf_tile_table(TableArgs a) {
       vd = __dadd_rn(vd, __shfl_xor_sync(0xffffffffu, vd, d));
     }
     if (lane == 0) {
-      double ex = __ddiv_rn(vx, vd);
-      double ey = __ddiv_rn(vy, vd);
-      if constexpr (MODE == M_FP16) {
-        ex = __dmul_rn(ex, 1.0 / 1024.0);
-        ey = __dmul_rn(ey, 1.0 / 1024.0);
+      s_last = 1;
+      if (nc > 1) {
+        double* rt = a.roots + ((size_t)track * nc + chunk) * 3;
+        rt[0] = vx;
+        rt[1] = vy;
+        rt[2] = vd;
+        __threadfence();
+        s_last = atomicAdd(sy + 3, 1ULL) == (unsigned long long)(nc - 1) ? 1 : 0;
       }
-      double* tr = a.traj + ((size_t)track * a.traj_stride + a.traj_index) * 2;
-      tr[0] = ex;
-      tr[1] = ey;
-      a.u_out[track] = u;
-      if (!(vd > 0.0) || !isfinite(vd) || !isfinite(ex) || !isfinite(ey)) atomicMin(a.degenerate + track, a.t);
+    }
+  }
+  __syncthreads();
+  if (!s_last) return;
+  if (nc > 1) {  // last CTA: tree over the chunk roots (power-of-two padded)
+    __threadfence();
+    const double* rt = a.roots + (size_t)track * nc * 3;
+    int ncp = 1;
+    while (ncp < nc) ncp <<= 1;
+    // each thread folds a contiguous pow2 block of chunk roots, then butterflies
+    const int per = max(1, ncp / TPB);
+    double px = 0.0, py = 0.0, pd = 0.0;
+    if (tid * per < ncp) {  // binary-counter pairwise fold of a pow2 block
+      PwAcc ax, ay, ad;
+      ax.reset();
+      ay.reset();
+      ad.reset();
+      for (int e = 0; e < per; ++e) {
+        const int c = tid * per + e;
+        ax.push(c < nc ? __ldcg(rt + 3 * c) : 0.0);
+        ay.push(c < nc ? __ldcg(rt + 3 * c + 1) : 0.0);
+        ad.push(c < nc ? __ldcg(rt + 3 * c + 2) : 0.0);
+      }
+      px = ax.root();
+      py = ay.root();
+      pd = ad.root();
+    }
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      px = __dadd_rn(px, __shfl_xor_sync(0xffffffffu, px, d));
+      py = __dadd_rn(py, __shfl_xor_sync(0xffffffffu, py, d));
+      pd = __dadd_rn(pd, __shfl_xor_sync(0xffffffffu, pd, d));
+    }
+    __syncthreads();
+    if (lane == 0) {
+      s_d[wid] = px;
+      s_d[32 + wid] = py;
+      s_d[64 + wid] = pd;
+    }
+    __syncthreads();
+    if (wid == 0) {
+      vx = lane < nw ? s_d[lane] : 0.0;
+      vy = lane < nw ? s_d[32 + lane] : 0.0;
+      vd = lane < nw ? s_d[64 + lane] : 0.0;
+#pragma unroll
+      for (int d = 1; d < 32; d <<= 1) {
+        vx = __dadd_rn(vx, __shfl_xor_sync(0xffffffffu, vx, d));
+        vy = __dadd_rn(vy, __shfl_xor_sync(0xffffffffu, vy, d));
+        vd = __dadd_rn(vd, __shfl_xor_sync(0xffffffffu, vd, d));
+      }
+    }
+  }
+  if (tid == 0) {
+    double ex = __ddiv_rn(vx, vd);
+    double ey = __ddiv_rn(vy, vd);
+    if constexpr (MODE == M_FP16) {
+      ex = __dmul_rn(ex, 1.0 / 1024.0);
+      ey = __dmul_rn(ey, 1.0 / 1024.0);
+    }
+    double* tr = a.traj + ((size_t)track * a.traj_stride + a.traj_index) * 2;
+    tr[0] = ex;
+    tr[1] = ey;
+    a.u_out[track] = u;
+    if (!(vd > 0.0) || !isfinite(vd) || !isfinite(ex) || !isfinite(ey)) atomicMin(a.degenerate + track, a.t);
+    if (nc > 1) {  // every CTA has passed both exchanges: reset for the next frame
+      sy[0] = 0;
+      sy[1] = 0;
+      sy[2] = 0;
+      sy[3] = 0;
+      __threadfence();
     }
   }
 }
