@@ -317,7 +317,11 @@ int pf_create(pf_handle** out, const pf_config* cfg) {
   h->n_tracks = cfg->n_tracks;
   h->n_videos = cfg->n_videos;
   // default threads per block per precision (measured, bench TPB sweep)
-  h->tpb = cfg->tpb ? cfg->tpb : (cfg->precision >= PF_FP16 ? 128 : 256);
+  // FP16 prefers 128 threads while the grid fits in about one wave, 256 beyond
+  {
+    const long long ctas = ((cfg->K + PF_TILE - 1) / PF_TILE) * (long long)cfg->n_tracks;
+    h->tpb = cfg->tpb ? cfg->tpb : (cfg->precision >= PF_FP16 && ctas <= 2048 ? 128 : 256);
+  }
   h->vpt = h->tpb >= 1024 ? 1 : h->tpb >= 512 ? 2 : h->tpb >= 256 ? 4 : 8;
   h->params = cfg->params;
   h->n_off = cfg->n_offsets;
@@ -337,8 +341,9 @@ int pf_create(pf_handle** out, const pf_config* cfg) {
   int lg = 0;
   while ((1LL << lg) < h->n_tiles) ++lg;
   h->Q = 52 - lg;
-  // tile table: one tile per thread; chunks of 128 tiles per CTA when n > 128
-  h->tpb_table = h->n_pad <= 128 ? std::max(32, h->n_pad) : 128;
+  // tile table: one tile per thread; a single CTA up to 1024 tiles (the
+  // cross-CTA exchanges cost more than they save there), chunks of 256 above
+  h->tpb_table = h->n_pad <= 1024 ? std::max(32, h->n_pad) : 256;
   h->n_chunks = (h->n_tiles + h->tpb_table - 1) / h->tpb_table;
   std::string& e = h->err;
 #define CK(x)                    \

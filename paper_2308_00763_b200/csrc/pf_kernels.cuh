@@ -1148,7 +1148,7 @@ __device__ __forceinline__ void spin_until(unsigned long long* ctr, unsigned lon
 // track are co-resident: each calls launch_dependents on entry, so the next
 // (dependent) grid cannot occupy the GPU before every table CTA has started.
 template <int MODE>
-__global__ void __launch_bounds__(128) pf_tile_table(TableArgs a) {
+__global__ void __launch_bounds__(1024) pf_tile_table(TableArgs a) {
   __shared__ long long s_i[32];
   __shared__ double s_d[3 * 32 + 4];
   __shared__ int s_last;
