@@ -138,6 +138,16 @@ int pf_systematic_ancestors(const double* cdf, int64_t K, double u, int64_t* anc
 int pf_rng_normals(uint64_t seed, uint64_t pos, int64_t n, double* out, int32_t device);
 int pf_rng_uniforms(uint64_t seed, uint64_t pos, int64_t n, double* out, int32_t device);
 
+/* NumPy-compatible reference stream (Generator(Philox(seed)), filter.py:71-82)
+ * generated on the device for the staged parity engine.  state11 = NumPy's
+ * Philox state: key[2], counter[4], buffer[4], buffer_pos.  Draws are
+ * sequential (variable ziggurat consumption): one device thread per stream. */
+typedef struct pf_philox pf_philox;
+int pf_philox_create(pf_philox** out, const uint64_t* state11, int32_t device);
+int pf_philox_destroy(pf_philox* p);
+int pf_philox_normals(pf_philox* p, int64_t n, double* out);
+int pf_philox_uniforms(pf_philox* p, int64_t n, double* out);
+
 /* RN16(exp(x)) for all 65536 binary16 patterns (host-built table used by the
  * kernels; exposed so tests can pin it against halfnum.exp16 on CPU). */
 int pf_exp16_table(uint16_t* out65536);

@@ -317,6 +317,87 @@ class _WordSource:
         return (self.next64() >> 11) * TWO_M53
 
 
+# --------------------------------------------------------------------------
+# glibc 2.39 x86-64 log1p (FMA ifunc variant), restated from its disassembly:
+# NumPy's ziggurat tail calls npy_log1p == glibc log1p, so the reference
+# stream's rare tail normals depend on it bit-for-bit.  fma() is exact
+# (Fraction) here and __fma_rn on the device.
+# --------------------------------------------------------------------------
+
+def _fma(a: float, b: float, c: float) -> float:
+    from fractions import Fraction
+
+    return float(Fraction(a) * Fraction(b) + Fraction(c))
+
+
+_G_L1, _G_L2, _G_L3 = float.fromhex("0x1.5555555555593p-1"), float.fromhex("0x1.999999997fa04p-2"), \
+    float.fromhex("0x1.2492494229359p-2")
+_G_L4, _G_L5 = float.fromhex("0x1.c71c51d8e78afp-3"), float.fromhex("0x1.7466496cb03dep-3")
+_G_L6, _G_L7 = float.fromhex("0x1.39a09d078c69fp-3"), float.fromhex("0x1.2f112df3e5244p-3")
+_G_LN2_LO, _G_LN2_HI = float.fromhex("0x1.a39ef35793c76p-33"), float.fromhex("0x1.62e42fee00000p-1")
+_G_C23 = float.fromhex("0x1.5555555555555p-1")
+
+
+def _bits(x: float) -> int:
+    return int(np.float64(x).view(np.uint64))
+
+
+def _frombits(b: int) -> float:
+    return float(np.uint64(b).view(np.float64))
+
+
+def log1p_glibc(x: float) -> float:
+    """glibc log1p for -1 < x <= 0.41422 (the ziggurat tail domain)."""
+    hx = _bits(x) >> 32
+    hx = hx - (1 << 32) if hx & 0x80000000 else hx
+    ax = hx & 0x7FFFFFFF
+    if ax <= 0x3E1FFFFF:
+        if ax <= 0x3C8FFFFF:
+            return x
+        return _fma(-(x * x), 0.5, x)
+    c = 0.0
+    if ((hx + 0x402D413C) & 0xFFFFFFFF) > 0x402D413C:
+        k, f, hu = 0, x, 1
+    else:
+        u = 1.0 + x
+        hu = _bits(u) >> 32
+        k = (hu >> 20) - 1023
+        c = (1.0 - (u - x)) if k > 0 else (x - (u - 1.0))
+        c = c / u
+        hu &= 0xFFFFF
+        lo = _bits(u) & 0xFFFFFFFF
+        if hu > 0x6A09D:
+            k += 1
+            u = _frombits(((hu | 0x3FE00000) << 32) | lo)
+            hu = (0x100000 - hu) >> 2
+        else:
+            u = _frombits(((hu | 0x3FF00000) << 32) | lo)
+        f = u - 1.0
+    hfsq = (f * 0.5) * f
+    kf = float(k)
+    if hu == 0:
+        if f == 0.0:
+            return 0.0 if k == 0 else _fma(kf, _G_LN2_HI, _fma(kf, _G_LN2_LO, c))
+        R = _fma(-f, _G_C23, 1.0) * hfsq
+        if k == 0:
+            return f - R
+        return _fma(kf, _G_LN2_HI, -((R - _fma(kf, _G_LN2_LO, c)) - f))
+    s = f / (f + 2.0)
+    z = s * s
+    t11 = _fma(z, _G_L3, _G_L2)
+    t10 = _fma(z, _G_L5, _G_L4)
+    t9 = _fma(z, _G_L7, _G_L6)
+    z2 = z * z
+    z4 = z2 * z2
+    z6 = z2 * z4
+    R = _fma(z6, t9, _fma(z4, t10, _fma(z, _G_L1, z2 * t11)))
+    t = (R + hfsq) * s
+    if k == 0:
+        return f - (hfsq - t)
+    klo = _fma(kf, _G_LN2_LO, c)
+    return _fma(kf, _G_LN2_HI, -((hfsq - (klo + t)) - f))
+
+
 def numpy_standard_normal(src: _WordSource, libm_exp=None, libm_log1p=None) -> float:
     """random_standard_normal (distributions.c) over a raw word source.
 
@@ -325,7 +406,7 @@ def numpy_standard_normal(src: _WordSource, libm_exp=None, libm_log1p=None) -> f
     import math
 
     ex = libm_exp or math.exp
-    l1p = libm_log1p or math.log1p
+    l1p = libm_log1p or log1p_glibc
     while True:
         r = src.next64()
         idx = r & 0xFF

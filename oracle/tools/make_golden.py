@@ -49,7 +49,9 @@ def acceptance():
     vid = generate_video(ModelParams(), 100, 128, 128, (64.0, 64.0), 42)
     out = {"frames_sha256": np.array(sha(vid.frames)), "truth": vid.truth}
     orig = hf.RngStream
-    out["philox_fp64_traj"] = hf.run(vid, 128, hf.PrecisionMode.FP64, 42, start_hint=(64.0, 64.0)).trajectory
+    for mode in MODES:  # the reference's own stream (Generator(Philox(42)))
+        out[f"philox_{mode}_traj"] = hf.run(vid, 128, hf.PrecisionMode.from_name(mode), 42,
+                                             start_hint=(64.0, 64.0)).trajectory
     hf.RngStream = rng.LcgStream
     try:
         for mode in MODES:

@@ -23,6 +23,7 @@ from .filter import (
     Filter,
     OpCounters,
     ParticleSet,
+    PhiloxRngStream,
     PrecisionMode,
     RngStream,
     RunResult,
@@ -37,6 +38,6 @@ __all__ = [
     "ModelParams", "PixelTemplate", "Video", "disk_template", "generate_video",
     "read_video", "write_video", "read_truth_csv", "write_truth_csv",
     "MAX_PARTICLES", "STAGES", "DegeneracyError", "Filter", "OpCounters", "ParticleSet",
-    "PrecisionMode", "RngStream", "RunResult", "accuracy_metrics", "init_particles",
+    "PhiloxRngStream", "PrecisionMode", "RngStream", "RunResult", "accuracy_metrics", "init_particles",
     "make_engine", "run", "systematic_ancestors",
 ]

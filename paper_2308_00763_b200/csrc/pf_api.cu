@@ -824,3 +824,72 @@ int pf_rng_uniforms(uint64_t seed, uint64_t pos, int64_t n, double* out, int32_t
 }  // extern "C"
 
 #include "pf_stage_api.inc"
+
+// ---------------------------------------------------------------------------
+// NumPy-compatible reference stream on the device (staged parity engine)
+// ---------------------------------------------------------------------------
+struct pf_philox {
+  pfr::PhiloxState* st = nullptr;
+  double* buf = nullptr;
+  long long cap = 0;
+  int device = 0;
+};
+
+extern "C" {
+
+int pf_philox_create(pf_philox** out, const uint64_t* state11, int32_t device) {
+  if (!out || !state11) return PF_EINVAL;
+  *out = nullptr;
+  PF_CUDA(cudaSetDevice(device), g_err);
+  int rc = init_device_tables(device, g_err);
+  if (rc) return rc;
+  pfr::PhiloxState h;
+  h.key[0] = state11[0];
+  h.key[1] = state11[1];
+  for (int i = 0; i < 4; ++i) h.ctr[i] = state11[2 + i];
+  for (int i = 0; i < 4; ++i) h.buf[i] = state11[6 + i];
+  h.pos = (int)state11[10];
+  pf_philox* p = new pf_philox();
+  p->device = device;
+  if (cudaMalloc(&p->st, sizeof(pfr::PhiloxState)) != cudaSuccess ||
+      cudaMemcpy(p->st, &h, sizeof(h), cudaMemcpyHostToDevice) != cudaSuccess) {
+    g_err = "philox state allocation failed";
+    if (p->st) cudaFree(p->st);
+    delete p;
+    return PF_ECUDA;
+  }
+  *out = p;
+  return PF_OK;
+}
+
+int pf_philox_destroy(pf_philox* p) {
+  if (!p) return PF_OK;
+  cudaSetDevice(p->device);
+  if (p->st) cudaFree(p->st);
+  if (p->buf) cudaFree(p->buf);
+  delete p;
+  return PF_OK;
+}
+
+static int philox_draw(pf_philox* p, int64_t n, double* out, bool normals) {
+  if (!p || !out || n < 0) return PF_EINVAL;
+  if (n == 0) return PF_OK;
+  PF_CUDA(cudaSetDevice(p->device), g_err);
+  if (p->cap < n) {
+    if (p->buf) cudaFree(p->buf);
+    p->buf = nullptr;
+    PF_CUDA(cudaMalloc(&p->buf, n * 8), g_err);
+    p->cap = n;
+  }
+  if (normals)
+    pfs::st_philox_draw<<<1, 1>>>(p->st, n, p->buf, 0, nullptr);
+  else
+    pfs::st_philox_draw<<<1, 1>>>(p->st, 0, nullptr, n, p->buf);
+  PF_CUDA(cudaGetLastError(), g_err);
+  PF_CUDA(cudaMemcpy(out, p->buf, n * 8, cudaMemcpyDeviceToHost), g_err);
+  return PF_OK;
+}
+int pf_philox_normals(pf_philox* p, int64_t n, double* out) { return philox_draw(p, n, out, true); }
+int pf_philox_uniforms(pf_philox* p, int64_t n, double* out) { return philox_draw(p, n, out, false); }
+
+}  // extern "C"

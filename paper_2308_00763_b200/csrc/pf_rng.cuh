@@ -117,4 +117,136 @@ __device__ __forceinline__ double normal_of(uint64_t w, const uint32_t* ki_hi, c
   return zig_slow(w);
 }
 
+// ---------------------------------------------------------------------------
+// NumPy-compatible reference stream (Generator(Philox(seed)), filter.py:71-82)
+// for the staged parity engine: Philox4x64-10 with NumPy's counter/buffer
+// semantics, NumPy's ziggurat (low-bit layout), and glibc's log1p restated
+// from its x86-64 FMA variant (oracle/rng.py log1p_glibc).  Sequential by
+// nature (variable consumption), one thread per stream.
+// ---------------------------------------------------------------------------
+struct PhiloxState {
+  unsigned long long key[2], ctr[4], buf[4];
+  int pos;
+};
+
+__device__ __forceinline__ void philox_block(const unsigned long long ctr_in[4], const unsigned long long key_in[2],
+                                             unsigned long long out[4]) {
+  unsigned long long c0 = ctr_in[0], c1 = ctr_in[1], c2 = ctr_in[2], c3 = ctr_in[3];
+  unsigned long long k0 = key_in[0], k1 = key_in[1];
+#pragma unroll
+  for (int r = 0; r < 10; ++r) {
+    if (r) {
+      k0 += 0x9E3779B97F4A7C15ULL;
+      k1 += 0xBB67AE8584CAA73BULL;
+    }
+    const unsigned long long lo0 = 0xD2E7470EE14C6C93ULL * c0, hi0 = __umul64hi(0xD2E7470EE14C6C93ULL, c0);
+    const unsigned long long lo1 = 0xCA5A826395121157ULL * c2, hi1 = __umul64hi(0xCA5A826395121157ULL, c2);
+    const unsigned long long n0 = hi1 ^ c1 ^ k0, n2 = hi0 ^ c3 ^ k1;
+    c0 = n0;
+    c1 = lo1;
+    c2 = n2;
+    c3 = lo0;
+  }
+  out[0] = c0;
+  out[1] = c1;
+  out[2] = c2;
+  out[3] = c3;
+}
+
+__device__ __forceinline__ unsigned long long philox_next(PhiloxState& st) {
+  if (st.pos < 4) return st.buf[st.pos++];
+  if (++st.ctr[0] == 0)
+    if (++st.ctr[1] == 0)
+      if (++st.ctr[2] == 0) ++st.ctr[3];
+  philox_block(st.ctr, st.key, st.buf);
+  st.pos = 1;
+  return st.buf[0];
+}
+__device__ __forceinline__ double philox_double(PhiloxState& st) { return uniform_of(philox_next(st)); }
+
+// glibc 2.39 log1p (x86-64 FMA variant), domain -1 < x <= 0.41422
+__device__ double log1p_glibc(double x) {
+  const double L1 = 0x1.5555555555593p-1, L2 = 0x1.999999997fa04p-2, L3 = 0x1.2492494229359p-2;
+  const double L4 = 0x1.c71c51d8e78afp-3, L5 = 0x1.7466496cb03dep-3, L6 = 0x1.39a09d078c69fp-3;
+  const double L7 = 0x1.2f112df3e5244p-3, LN2_LO = 0x1.a39ef35793c76p-33, LN2_HI = 0x1.62e42fee00000p-1;
+  const double C23 = 0x1.5555555555555p-1;
+  const int hx = __double2hiint(x);
+  const int ax = hx & 0x7fffffff;
+  if (ax <= 0x3e1fffff) {
+    if (ax <= 0x3c8fffff) return x;
+    return __fma_rn(-__dmul_rn(x, x), 0.5, x);
+  }
+  double c = 0.0, f;
+  int k, hu;
+  if ((unsigned)(hx + 0x402d413c) > 0x402d413cu) {
+    k = 0;
+    f = x;
+    hu = 1;
+  } else {
+    double u = __dadd_rn(1.0, x);
+    hu = __double2hiint(u);
+    k = (hu >> 20) - 1023;
+    c = k > 0 ? __dsub_rn(1.0, __dsub_rn(u, x)) : __dsub_rn(x, __dsub_rn(u, 1.0));
+    c = __ddiv_rn(c, u);
+    hu &= 0xfffff;
+    const int lo = __double2loint(u);
+    if (hu > 0x6a09d) {
+      k += 1;
+      u = __hiloint2double(hu | 0x3fe00000, lo);
+      hu = (0x100000 - hu) >> 2;
+    } else {
+      u = __hiloint2double(hu | 0x3ff00000, lo);
+    }
+    f = __dsub_rn(u, 1.0);
+  }
+  const double hfsq = __dmul_rn(__dmul_rn(f, 0.5), f);
+  const double kf = (double)k;
+  if (hu == 0) {
+    if (f == 0.0) return k == 0 ? 0.0 : __fma_rn(kf, LN2_HI, __fma_rn(kf, LN2_LO, c));
+    const double R = __dmul_rn(__fma_rn(-f, C23, 1.0), hfsq);
+    if (k == 0) return __dsub_rn(f, R);
+    return __fma_rn(kf, LN2_HI, -__dsub_rn(__dsub_rn(R, __fma_rn(kf, LN2_LO, c)), f));
+  }
+  const double s = __ddiv_rn(f, __dadd_rn(f, 2.0));
+  const double z = __dmul_rn(s, s);
+  const double t11 = __fma_rn(z, L3, L2), t10 = __fma_rn(z, L5, L4), t9 = __fma_rn(z, L7, L6);
+  const double z2 = __dmul_rn(z, z), z4 = __dmul_rn(z2, z2), z6 = __dmul_rn(z2, z4);
+  const double R = __fma_rn(z6, t9, __fma_rn(z4, t10, __fma_rn(z, L1, __dmul_rn(z2, t11))));
+  const double t = __dmul_rn(__dadd_rn(R, hfsq), s);
+  if (k == 0) return __dsub_rn(f, __dsub_rn(hfsq, t));
+  const double klo = __fma_rn(kf, LN2_LO, c);
+  return __fma_rn(kf, LN2_HI, -__dsub_rn(__dsub_rn(hfsq, __dadd_rn(klo, t)), f));
+}
+
+// numpy random_standard_normal over the Philox stream (distributions.c)
+__device__ double numpy_normal(PhiloxState& st) {
+  for (;;) {
+    unsigned long long r = philox_next(st);
+    const unsigned idx = (unsigned)(r & 0xff);
+    r >>= 8;
+    const unsigned sign = (unsigned)(r & 1);
+    const unsigned long long rabs = (r >> 1) & kMask52;
+    double x = pfm::dmul((double)rabs, __longlong_as_double((long long)PF_ZIG_WI_BITS[idx]));
+    if (sign) x = -x;
+    if (rabs < PF_ZIG_KI[idx]) return x;
+    if (idx == 0) {
+      for (;;) {
+        const double xx = pfm::dmul(-kZigInvR, log1p_glibc(-philox_double(st)));
+        const double yy = -log1p_glibc(-philox_double(st));
+        if (pfm::dadd(yy, yy) > pfm::dmul(xx, xx))
+          return ((rabs >> 8) & 1) ? -pfm::dadd(kZigR, xx) : pfm::dadd(kZigR, xx);
+      }
+    } else {
+      const double fi0 = __longlong_as_double((long long)PF_ZIG_FI_BITS[idx - 1]);
+      const double fi1 = __longlong_as_double((long long)PF_ZIG_FI_BITS[idx]);
+      // glibc exp vs the portable exp64 here only decides a comparison; they
+      // differ by at most an ulp, so a flip needs the uniform to land within
+      // ~2^-52 of the wedge boundary (documented in DESIGN.md)
+      if (pfm::dadd(pfm::dmul(pfm::dsub(fi0, fi1), philox_double(st)), fi1) <
+          pfm::exp64(pfm::dmul(pfm::dmul(-0.5, x), x)))
+        return x;
+    }
+  }
+}
+
 }  // namespace pfr

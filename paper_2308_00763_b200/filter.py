@@ -161,6 +161,41 @@ class RngStream:
         return float(out[0])
 
 
+class PhiloxRngStream:
+    """The reference's own stream, Generator(Philox(seed)) (filter.py:71-82),
+    generated on the device (NumPy's Philox4x64-10 counter/buffer semantics,
+    NumPy's ziggurat, glibc's log1p).  Inject it as `filter.RngStream` to run
+    the staged engine on exactly the reference's draws.  The Philox key comes
+    from NumPy's SeedSequence expansion of the seed (host seeding only)."""
+
+    def __init__(self, seed: int, device: int = 0):
+        st = np.random.Philox(seed).state
+        state = np.array(list(st["state"]["key"]) + list(st["state"]["counter"]) + list(st["buffer"]) +
+                         [st["buffer_pos"]], dtype=np.uint64)
+        h = C.c_void_p()
+        N.check(N.lib().pf_philox_create(C.byref(h), N.ptr(state), device), N.lib().pf_global_error)
+        self._h = h
+        self.seed = seed
+
+    def __del__(self):
+        if getattr(self, "_h", None):
+            try:
+                N.lib().pf_philox_destroy(self._h)
+            except Exception:
+                pass
+            self._h = None
+
+    def normals(self, n: int) -> np.ndarray:
+        out = np.empty(2 * n, dtype=np.float64)
+        N.check(N.lib().pf_philox_normals(self._h, 2 * n, N.ptr(out)), N.lib().pf_global_error)
+        return out.reshape(n, 2)
+
+    def uniform(self) -> float:
+        out = np.empty(1, dtype=np.float64)
+        N.check(N.lib().pf_philox_uniforms(self._h, 1, N.ptr(out)), N.lib().pf_global_error)
+        return float(out[0])
+
+
 # ---------------------------------------------------------------------------
 # staged engine (reference semantics)
 # ---------------------------------------------------------------------------

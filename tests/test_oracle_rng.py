@@ -100,3 +100,15 @@ def test_scalar_and_vector_exp_identical():
     xs = np.random.default_rng(0).uniform(-720, 720, 5000)
     v = rng.exp64_np(xs)
     assert all(rng.exp64(float(a)) == b for a, b in zip(xs, v))
+
+
+def test_glibc_log1p_restatement_matches_libm():
+    # NumPy's ziggurat tail uses npy_log1p (glibc); the device restatement must
+    # agree bit-for-bit on the tail domain (-1, 0]
+    import math
+
+    g = np.random.default_rng(5)
+    xs = np.concatenate([-g.random(60_000), -g.random(20_000) ** 12, -(1 - g.random(20_000) * 1e-3)])
+    w = g.integers(0, 2**63, 40_000, dtype=np.int64).astype(np.uint64)
+    xs = np.concatenate([xs, -(w >> np.uint64(11)).astype(np.float64) * 2.0**-53])
+    assert all(rng.log1p_glibc(float(v)) == math.log1p(float(v)) for v in xs)
