@@ -151,6 +151,9 @@ int pf_philox_uniforms(pf_philox* p, int64_t n, double* out);
 /* RN16(exp(x)) for all 65536 binary16 patterns (host-built table used by the
  * kernels; exposed so tests can pin it against halfnum.exp16 on CPU). */
 int pf_exp16_table(uint16_t* out65536);
+/* The device's exp16 as used by the fused FP16 kernel (fast path + table
+ * fallback) for all 65536 inputs -- must equal pf_exp16_table on d <= 0. */
+int pf_exp16_device(uint16_t* out65536, int32_t device);
 
 #ifdef __cplusplus
 }

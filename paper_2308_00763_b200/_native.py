@@ -84,6 +84,7 @@ SIGNATURES = [
     ("pf_rng_normals", C.c_int, [C.c_uint64, C.c_uint64, C.c_int64, _VP, C.c_int32]),
     ("pf_rng_uniforms", C.c_int, [C.c_uint64, C.c_uint64, C.c_int64, _VP, C.c_int32]),
     ("pf_exp16_table", C.c_int, [_VP]),
+    ("pf_exp16_device", C.c_int, [_VP, C.c_int32]),
     ("pf_philox_create", C.c_int, [C.POINTER(_VP), _VP, C.c_int32]),
     ("pf_philox_destroy", C.c_int, [_VP]),
     ("pf_philox_normals", C.c_int, [_VP, C.c_int64, _VP]),

@@ -252,6 +252,23 @@ int pf_exp16_table(uint16_t* out) {
   return PF_OK;
 }
 
+int pf_exp16_device(uint16_t* out, int32_t device) {
+  if (!out) return PF_EINVAL;
+  PF_CUDA(cudaSetDevice(device), g_err);
+  std::vector<uint16_t> host(65536);
+  build_exp16(host.data());
+  unsigned short *tab = nullptr, *res = nullptr;
+  PF_CUDA(cudaMalloc(&tab, 65536 * 2), g_err);
+  PF_CUDA(cudaMalloc(&res, 65536 * 2), g_err);
+  PF_CUDA(cudaMemcpy(tab, host.data(), 65536 * 2, cudaMemcpyHostToDevice), g_err);
+  pfk::pf_exp16_fast_check<<<256, 256>>>(tab, res);
+  PF_CUDA(cudaGetLastError(), g_err);
+  PF_CUDA(cudaMemcpy(out, res, 65536 * 2, cudaMemcpyDeviceToHost), g_err);
+  cudaFree(tab);
+  cudaFree(res);
+  return PF_OK;
+}
+
 int pf_destroy(pf_handle* h) {
   if (!h) return PF_OK;
   cudaSetDevice(h->device);

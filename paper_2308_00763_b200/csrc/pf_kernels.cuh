@@ -443,11 +443,38 @@ __device__ __forceinline__ long long weight_q<M_FP32>(float L, float m, const un
   float w = pfm::exp32(__fsub_rn(L, m));
   return __float2ll_rn(__fmul_rn(w, 1099511627776.0f));  // 2^40
 }
+// RN16(exp(d)) for binary16 d <= 0, bit-identical to the correctly rounded
+// table: exp(d) = 0 in binary16 below -17.33; in [-9.70, 0] ex2.approx gives
+// y within ~2^-20 relative, so RN16(y) is the correctly rounded value unless
+// y's 13 bits below binary16 precision lie within a margin of the rounding
+// midpoint -- then (and in the subnormal range) read the table.  Checked
+// exhaustively against the table on the device (tests/test_gpu_fused.py).
+__device__ __forceinline__ __half exp16_fast(__half d, const unsigned short* exp16) {
+  const float x = __half2float(d);
+  if (x < -17.34f) return __ushort_as_half(0);
+  if (x >= -9.70f) {
+    float y;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(__fmul_rn(x, 1.44269504088896340736f)));
+    const unsigned low = __float_as_uint(y) & 0x1fffu;  // bits below binary16 precision
+    const int off = (int)low - 0x1000;
+    if (off > 48 || off < -48) return __float2half_rn(y);
+  }
+  return __ushort_as_half(__ldg(exp16 + __half_as_ushort(d)));
+}
+
 template <>
 __device__ __forceinline__ int weight_q<M_FP16>(__half L, __half m, const unsigned short* exp16) {
-  __half d = __hsub_rn(L, m);
-  __half w = __ushort_as_half(__ldg(exp16 + __half_as_ushort(d)));
+  const __half w = exp16_fast(__hsub_rn(L, m), exp16);
   return __float2int_rn(__fmul_rn(__half2float(w), 1048576.0f));  // 2^20
+}
+
+// exhaustive check helper: out[i] = exp16_fast(bits i) for all 65536 patterns
+__global__ void pf_exp16_fast_check(const unsigned short* exp16, unsigned short* out) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < 65536) {
+    const __half d = __ushort_as_half((unsigned short)i);
+    out[i] = (__half2float(d) <= 0.0f) ? __half_as_ushort(exp16_fast(d, exp16)) : exp16[i];
+  }
 }
 
 // search keys: c_j >= q  <=>  key(c_j) >= key_up(q) for non-negative values,
@@ -548,7 +575,13 @@ __device__ __forceinline__ typename Tr<MODE>::vec prop(typename Tr<MODE>::vec xa
 
 template <int MODE>
 constexpr int max_src_tiles() {  // source tiles staged in shared memory (else global search)
-  return MODE == M_FP64 ? 3 : 4;
+  return MODE == M_FP16 ? 3 : (MODE == M_FP64 ? 3 : 4);
+}
+// FP16 also stages the source tiles' positions (4 B each): the ancestor
+// gather becomes a shared-memory load
+template <int MODE>
+constexpr bool stage_positions() {
+  return MODE == M_FP16;
 }
 
 constexpr int kSlowQ = 128;  // deferred ziggurat slow paths per CTA (overflow -> inline)
@@ -560,6 +593,7 @@ constexpr size_t fused_smem_bytes() {
   using real = typename Tr<MODE>::real;
   using vec = typename Tr<MODE>::vec;
   return 3072 + PF_TILE * sizeof(vec) + max_src_tiles<MODE>() * PF_TILE * sizeof(real) +
+         (stage_positions<MODE>() ? max_src_tiles<MODE>() * PF_TILE * sizeof(vec) : 0) +
          (max_src_tiles<MODE>() + 1) * 24 + kSlowQ * 12 + 320 * 8;
 }
 
@@ -633,7 +667,9 @@ __global__ void __launch_bounds__(PF_TILE / (VPT * R)) pf_fused_frame(FusedArgs 
   double* s_wi = reinterpret_cast<double*>(smem + 1024);  // 2 KB
   vec* s_X = reinterpret_cast<vec*>(smem + 3072);  // per-particle noise
   real* s_c = reinterpret_cast<real*>(smem + 3072 + PF_TILE * sizeof(vec));
-  unsigned char* p_tab = reinterpret_cast<unsigned char*>(s_c + MS * PF_TILE);
+  vec* s_xp = reinterpret_cast<vec*>(s_c + MS * PF_TILE);  // staged source positions (FP16)
+  unsigned char* p_tab =
+      reinterpret_cast<unsigned char*>(stage_positions<MODE>() ? (void*)(s_xp + MS * PF_TILE) : (void*)(s_c + MS * PF_TILE));
   int* s_ts = reinterpret_cast<int*>(p_tab);                        // MS + 1 (in-track indices)
   double* s_tO = reinterpret_cast<double*>(p_tab + (MS + 1) * 8);   // MS + 1
   double* s_tM = reinterpret_cast<double*>(p_tab + (MS + 1) * 16);  // MS + 1
@@ -774,7 +810,7 @@ __global__ void __launch_bounds__(PF_TILE / (VPT * R)) pf_fused_frame(FusedArgs 
     b_lo = s_int[0];
     b_hi = s_int[1];
     staged = s_int[2];
-    if (staged) {  // 16-byte copies of exactly the source tiles' local CDFs
+    if (staged) {  // 16-byte copies of exactly the source tiles' local CDFs (+ positions)
       const int c0 = b_lo * PF_TILE;
       const int cnt = min((b_hi + 1) * PF_TILE, K) - c0;
       constexpr int PER = 16 / sizeof(real);
@@ -787,10 +823,23 @@ __global__ void __launch_bounds__(PF_TILE / (VPT * R)) pf_fused_frame(FusedArgs 
       } else {
         for (int i = tid; i < cnt; i += TPB) s_c[i] = Cp[c0 + i];
       }
+      if constexpr (stage_positions<MODE>()) {
+        constexpr int PV = 16 / sizeof(vec);
+        if ((((size_t)track * K) % PV) == 0) {
+          const int nvec = cnt / PV;
+          const uint4* src = reinterpret_cast<const uint4*>(Xp + c0);
+          uint4* dst = reinterpret_cast<uint4*>(s_xp);
+          for (int i = tid; i < nvec; i += TPB) dst[i] = __ldg(src + i);
+          for (int i = nvec * PV + tid; i < cnt; i += TPB) s_xp[i] = Xp[c0 + i];
+        } else {
+          for (int i = tid; i < cnt; i += TPB) s_xp[i] = Xp[c0 + i];
+        }
+      }
       __syncthreads();
     }
   }
   const real* Csrc = staged ? s_c - b_lo * PF_TILE : Cp;
+  const vec* Xsrc = (stage_positions<MODE>() && staged) ? s_xp - b_lo * PF_TILE : Xp;
   const double invK = __ddiv_rn(1.0, (double)K);
 
   vec drift, stdv;
@@ -882,7 +931,7 @@ __global__ void __launch_bounds__(PF_TILE / (VPT * R)) pf_fused_frame(FusedArgs 
     for (int i = 0; i < VPT; ++i) {
       const int l = l0 + i;
       if (l < Tb) {
-        const vec xn = prop<MODE>(Xp[anc[i]], s_X[l], drift, stdv);
+        const vec xn = prop<MODE>(Xsrc[anc[i]], s_X[l], drift, stdv);
         Xn[base + l] = xn;
         const int ix = round_clamp<MODE>(xn.x, -a.r, a.W - 1 + a.r);
         const int iy = round_clamp<MODE>(xn.y, -a.r, a.H - 1 + a.r);

@@ -45,6 +45,20 @@ def test_device_rng_matches_oracle(pf):
             assert np.array_equal(uo, (w >> np.uint64(11)).astype(np.float64) * rng.TWO_M53)
 
 
+def test_exp16_fast_path_equals_table_exhaustively(pf):
+    # the fused FP16 kernel's exp16 (ex2.approx + midpoint guard + table
+    # fallback) must equal RN16(exp(d)) for every binary16 d <= 0
+    from paper_2308_00763_b200 import _native as N
+
+    dev = np.empty(65536, dtype=np.uint16)
+    tab = np.empty(65536, dtype=np.uint16)
+    assert N.lib().pf_exp16_device(N.ptr(dev), 0) == 0
+    assert N.lib().pf_exp16_table(N.ptr(tab)) == 0
+    x = np.arange(65536, dtype=np.uint32).astype(np.uint16).view(np.float16).astype(np.float32)
+    sel = (x <= 0) & ~np.isnan(x)
+    assert np.array_equal(dev[sel], tab[sel])
+
+
 def test_device_rng_stream_class(pf):
     g = golden("lcg_stream.npz")
     s = pf.RngStream(42)
