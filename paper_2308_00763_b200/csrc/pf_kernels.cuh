@@ -575,13 +575,14 @@ __device__ __forceinline__ typename Tr<MODE>::vec prop(typename Tr<MODE>::vec xa
 
 template <int MODE>
 constexpr int max_src_tiles() {  // source tiles staged in shared memory (else global search)
-  return MODE == M_FP16 ? 3 : (MODE == M_FP64 ? 3 : 4);
+  return MODE == M_FP64 ? 3 : 4;
 }
-// FP16 also stages the source tiles' positions (4 B each): the ancestor
-// gather becomes a shared-memory load
+// staging the source tiles' positions as well (ancestor gather from shared
+// memory) was measured: slightly better latency at C2, worse at C3/C4 (it
+// copies every source position, not only the ancestors) -- off
 template <int MODE>
 constexpr bool stage_positions() {
-  return MODE == M_FP16;
+  return false;
 }
 
 constexpr int kSlowQ = 128;  // deferred ziggurat slow paths per CTA (overflow -> inline)
