@@ -101,6 +101,16 @@ int pf_last_timings(const pf_handle* h, float* ms6);
  * (events between launches on the handle's stream). */
 int pf_set_profiling(pf_handle* h, int32_t on);
 
+/* Timeline tracing (performance analysis): when on, thread 0 of every CTA of
+ * track 0 stamps %globaltimer (ns) at fixed points of the next runs:
+ * per frame f, (n_tiles + n_chunks) records of 8 uint64 -- fused tile b:
+ * [0] entry [1] draws done [2] predecessor released [3] window ready
+ * [4] particles done [5] exit; table chunk c: [0] entry [1] released
+ * [2] tree done [3] estimate written (last CTA only).  Unset slots are 0.
+ * pf_get_trace copies the first n uint64 of the last run's buffer. */
+int pf_set_trace(pf_handle* h, int32_t on);
+int pf_get_trace(pf_handle* h, uint64_t* out, int64_t n);
+
 /* Kernel launches issued by the last pf_run/pf_step. */
 int64_t pf_last_launches(const pf_handle* h);
 

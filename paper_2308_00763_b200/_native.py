@@ -65,6 +65,8 @@ SIGNATURES = [
     ("pf_set_profiling", C.c_int, [_VP, C.c_int32]),
     ("pf_last_timings", C.c_int, [_VP, C.POINTER(C.c_float)]),
     ("pf_last_launches", C.c_int64, [_VP]),
+    ("pf_set_trace", C.c_int, [_VP, C.c_int32]),
+    ("pf_get_trace", C.c_int, [_VP, _VP, C.c_int64]),
     ("pf_get_state", C.c_int, [_VP, C.c_int32, _VP, _VP, _VP]),
     ("pf_get_debug", C.c_int, [_VP, C.c_int32, _VP, _VP]),
     ("pf_stage_create", C.c_int, [C.POINTER(_VP), C.c_int32, C.c_int64, C.POINTER(pf_params), _VP, C.c_int32, C.c_int32]),

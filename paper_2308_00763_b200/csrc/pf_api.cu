@@ -154,6 +154,7 @@ struct pf_handle {
   long long *rec_S = nullptr, *rec_X = nullptr, *rec_Y = nullptr;
   long long* tab_s = nullptr;
   double *tab_O = nullptr, *tab_invM = nullptr, *u = nullptr;
+  int2* win = nullptr;  // [track][tile] source window for the next frame
   unsigned long long* x0 = nullptr;
   ulonglong2* tj = nullptr;
   ulonglong2* tt = nullptr;
@@ -189,6 +190,9 @@ struct pf_handle {
   int g_cur = -1, g_F = -1;
   const void* g_maps = nullptr;
   const void* g_traj = nullptr;
+  unsigned long long* d_trace = nullptr;  // pf_set_trace: [frame][n_tiles + n_chunks][8]
+  size_t trace_cap = 0;
+  bool tracing = false;
 };
 
 typedef void (*fused_fn)(pfk::FusedArgs);
@@ -273,8 +277,8 @@ int pf_destroy(pf_handle* h) {
   if (!h) return PF_OK;
   cudaSetDevice(h->device);
   void* ptrs[] = {h->X[0], h->X[1], h->C[0], h->C[1], h->rec_m, h->rec_S, h->rec_X, h->rec_Y, h->tab_s, h->tab_O,
-                  h->tab_invM, h->u, h->x0, h->tj, h->tt, h->tsync, h->tagg, h->troots, h->exp16, h->zig, h->d_offs, h->d_plan, h->d_leaves, h->d_frames,
-                  h->d_maps, h->d_traj, h->d_degen, h->dbg_anc, h->dbg_L};
+                  h->tab_invM, h->win, h->u, h->x0, h->tj, h->tt, h->tsync, h->tagg, h->troots, h->exp16, h->zig, h->d_offs, h->d_plan, h->d_leaves, h->d_frames,
+                  h->d_maps, h->d_traj, h->d_degen, h->dbg_anc, h->dbg_L, h->d_trace};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   for (auto& e : h->ev)
@@ -387,7 +391,7 @@ int pf_create(pf_handle** out, const pf_config* cfg) {
   const size_t NT = (size_t)h->n_tiles * h->n_tracks;
   for (int i = 0; i < 2; ++i) {
     CK(cudack(cudaMalloc(&h->X[i], KT * h->vs), "X"));
-    CK(cudack(cudaMalloc(&h->C[i], KT * h->rs), "C"));
+    CK(cudack(cudaMalloc(&h->C[i], KT * h->rs + 16), "C"));  // slack: 16-byte rounded bulk copies
   }
   CK(cudack(cudaMalloc(&h->rec_m, NT * 8), "rec"));
   CK(cudack(cudaMalloc(&h->rec_S, NT * 8), "rec"));
@@ -396,6 +400,7 @@ int pf_create(pf_handle** out, const pf_config* cfg) {
   CK(cudack(cudaMalloc(&h->tab_s, NT * 8), "tab"));
   CK(cudack(cudaMalloc(&h->tab_O, NT * 8), "tab"));
   CK(cudack(cudaMalloc(&h->tab_invM, NT * 8), "tab"));
+  CK(cudack(cudaMalloc(&h->win, NT * sizeof(int2)), "win"));
   CK(cudack(cudaMalloc(&h->u, h->n_tracks * 8), "u"));
   CK(cudack(cudaMalloc(&h->d_degen, h->n_tracks * sizeof(int)), "degen"));
   CK(cudack(cudaMalloc(&h->tsync, (size_t)h->n_tracks * 4 * 8), "tsync"));
@@ -585,6 +590,11 @@ static int launch_frame(pf_handle* h, const void* map_slot, long long map_video_
   a.fa = ff.a;
   a.fc = ff.c;
   a.tt = h->tt;
+  a.win = h->win;
+  a.tmax = h->tsync;
+  a.ready_target = (unsigned long long)h->n_chunks * (unsigned long long)h->frame_counter;
+  const size_t tr_frame = (size_t)(h->n_tiles + h->n_chunks) * 8;
+  a.trace = h->tracing ? h->d_trace + (size_t)traj_index * tr_frame : nullptr;
   PF_CUDA(launch_pdl(h, (const void*)fused_kernel(h), dim3(h->n_tiles, h->n_tracks), dim3(h->tpb), h->fused_smem, a),
           h->err);
   PF_CUDA(cudaGetLastError(), h->err);
@@ -618,6 +628,8 @@ static int launch_frame(pf_handle* h, const void* map_slot, long long map_video_
   t.sync = h->tsync;
   t.agg = h->tagg;
   t.roots = h->troots;
+  t.win = h->win;
+  t.trace = h->tracing ? h->d_trace + (size_t)traj_index * tr_frame + (size_t)h->n_tiles * 8 : nullptr;
   PF_CUDA(launch_pdl(h, tk, dim3(h->n_chunks, h->n_tracks), dim3(h->tpb_table), 0, t), h->err);
   PF_CUDA(cudaGetLastError(), h->err);
   if (h->profiling) PF_CUDA(cudaEventRecord(h->pev[3 * traj_index + 2], h->stream), h->err);
@@ -649,6 +661,12 @@ int pf_run(pf_handle* h, const uint8_t* frames, int32_t F, int32_t on_device, do
   int rc;
   if ((rc = grow((void**)&h->d_maps, &h->maps_cap, (size_t)h->n_videos * F * map_elems * h->rs, h->err))) return rc;
   if ((rc = grow((void**)&h->d_traj, &h->traj_cap, (size_t)h->n_tracks * F * 2 * 8, h->err))) return rc;
+  if (h->tracing) {
+    const size_t need = (size_t)F * (h->n_tiles + h->n_chunks) * 8 * 8;
+    if (h->trace_cap < need) h->g_F = -1;  // re-capture with the new buffer
+    if ((rc = grow((void**)&h->d_trace, &h->trace_cap, need, h->err))) return rc;
+    PF_CUDA(cudaMemsetAsync(h->d_trace, 0, need, h->stream), h->err);
+  }
   if (h->profiling) {
     while ((int)h->pev.size() < 3 * F) {
       cudaEvent_t e;
@@ -745,6 +763,22 @@ int pf_degenerate_frame(const pf_handle* h) { return h ? h->degenerate_frame : -
 int pf_set_profiling(pf_handle* h, int32_t on) {
   if (!h) return PF_EINVAL;
   h->profiling = on != 0;
+  return PF_OK;
+}
+
+int pf_set_trace(pf_handle* h, int32_t on) {
+  if (!h) return PF_EINVAL;
+  if ((on != 0) != h->tracing) h->g_F = -1;  // kernel arguments change: re-capture
+  h->tracing = on != 0;
+  return PF_OK;
+}
+
+int pf_get_trace(pf_handle* h, uint64_t* out, int64_t n) {
+  if (!h || !out || n < 0) return PF_EINVAL;
+  PF_CUDA(cudaSetDevice(h->device), h->err);
+  PF_CUDA(cudaStreamSynchronize(h->stream), h->err);
+  if ((size_t)n * 8 > h->trace_cap) return PF_EINVAL;
+  PF_CUDA(cudaMemcpy(out, h->d_trace, (size_t)n * 8, cudaMemcpyDeviceToHost), h->err);
   return PF_OK;
 }
 

@@ -304,7 +304,33 @@ struct FusedArgs {
   const void* zig;     // packed ziggurat fast-path tables: ki>>20 (u32 x 256) then wi (f64 x 256)
   unsigned long long fa, fc;  // f^(t(2K+1)): frame base state = fa * x0[track] + fc
   const ulonglong2* tt;       // per tile: f^(2 * tile * PF_TILE)
+  const void* win;            // [track][tile] int2: first / last source tile (tile table of the previous frame)
+  unsigned long long* tmax;   // per track (stride 4): [0] order key of the running max of the tile maxima,
+                              //   [1] table-ready counter (+1 per table chunk and frame)
+  unsigned long long ready_target;  // frame t > 0 proceeds once tmax[1] >= this (n_chunks * t)
+  unsigned long long* trace;  // optional: [tile][8] %globaltimer stamps (track 0)
 };
+
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#define PF_TRACE(A, SLOT)                                                   \
+  do {                                                                      \
+    if ((A).trace != nullptr && threadIdx.x == 0 && blockIdx.y == 0)        \
+      (A).trace[(size_t)blockIdx.x * 8 + (SLOT)] = gtimer();                \
+  } while (0)
+
+// order-preserving map double -> uint64 (for atomicMax); 0 is below every key
+__device__ __forceinline__ unsigned long long okey(double d) {
+  const unsigned long long b = (unsigned long long)__double_as_longlong(d);
+  return (b & 0x8000000000000000ULL) ? ~b : (b | 0x8000000000000000ULL);
+}
+__device__ __forceinline__ double okey_inv(unsigned long long k) {
+  const unsigned long long b = (k & 0x8000000000000000ULL) ? (k & 0x7fffffffffffffffULL) : ~k;
+  return __longlong_as_double((long long)b);
+}
 
 // Programmatic dependent launch: let the next kernel in the stream start
 // early, and wait for the previous kernel's results only where they are
@@ -462,9 +488,14 @@ __device__ __forceinline__ __half exp16_fast(__half d, const unsigned short* exp
   return __ushort_as_half(__ldg(exp16 + __half_as_ushort(d)));
 }
 
+// FP16 weights read the correctly rounded table directly (L1-resident: only
+// the ~19.5K patterns in [-17.34, 0] are ever touched); kExp16Fast selects the
+// ex2.approx + midpoint-guard path instead (same bits, more instructions)
+constexpr bool kExp16Fast = false;
 template <>
 __device__ __forceinline__ int weight_q<M_FP16>(__half L, __half m, const unsigned short* exp16) {
-  const __half w = exp16_fast(__hsub_rn(L, m), exp16);
+  const __half d = __hsub_rn(L, m);
+  const __half w = kExp16Fast ? exp16_fast(d, exp16) : __ushort_as_half(__ldg(exp16 + __half_as_ushort(d)));
   return __float2int_rn(__fmul_rn(__half2float(w), 1048576.0f));  // 2^20
 }
 
@@ -556,19 +587,20 @@ __device__ __forceinline__ typename Tr<MODE>::vec to_vec(double n0, double n1) {
   return v;
 }
 
-// propagate with the noise already in the mode dtype (reference arithmetic)
+// propagate with the scaled noise sn = d(std) * d(n) already formed:
+// x' = (x[a] + d(drift)) + sn, each op rounded separately (reference arithmetic)
 template <int MODE>
-__device__ __forceinline__ typename Tr<MODE>::vec prop(typename Tr<MODE>::vec xa, typename Tr<MODE>::vec nn,
-                                                       typename Tr<MODE>::vec drift, typename Tr<MODE>::vec stdv) {
+__device__ __forceinline__ typename Tr<MODE>::vec prop(typename Tr<MODE>::vec xa, typename Tr<MODE>::vec sn,
+                                                       typename Tr<MODE>::vec drift) {
   typename Tr<MODE>::vec o;
   if constexpr (MODE == M_FP16) {
-    o = __hadd2_rn(__hadd2_rn(xa, drift), __hmul2_rn(stdv, nn));
+    o = __hadd2_rn(__hadd2_rn(xa, drift), sn);
   } else if constexpr (MODE == M_FP32) {
-    o.x = __fadd_rn(__fadd_rn(xa.x, drift.x), __fmul_rn(stdv.x, nn.x));
-    o.y = __fadd_rn(__fadd_rn(xa.y, drift.y), __fmul_rn(stdv.y, nn.y));
+    o.x = __fadd_rn(__fadd_rn(xa.x, drift.x), sn.x);
+    o.y = __fadd_rn(__fadd_rn(xa.y, drift.y), sn.y);
   } else {
-    o.x = __dadd_rn(__dadd_rn(xa.x, drift.x), __dmul_rn(stdv.x, nn.x));
-    o.y = __dadd_rn(__dadd_rn(xa.y, drift.y), __dmul_rn(stdv.y, nn.y));
+    o.x = __dadd_rn(__dadd_rn(xa.x, drift.x), sn.x);
+    o.y = __dadd_rn(__dadd_rn(xa.y, drift.y), sn.y);
   }
   return o;
 }
@@ -577,13 +609,9 @@ template <int MODE>
 constexpr int max_src_tiles() {  // source tiles staged in shared memory (else global search)
   return MODE == M_FP64 ? 3 : 4;
 }
-// staging the source tiles' positions as well (ancestor gather from shared
-// memory) was measured: slightly better latency at C2, worse at C3/C4 (it
-// copies every source position, not only the ancestors) -- off
-template <int MODE>
-constexpr bool stage_positions() {
-  return false;
-}
+// (staging the source tiles' positions as well -- ancestor gather from shared
+// memory -- was measured: slightly better latency at C2, worse at C3/C4 since
+// it copies every source position, not only the ancestors; not done)
 
 constexpr int kSlowQ = 128;  // deferred ziggurat slow paths per CTA (overflow -> inline)
 
@@ -593,8 +621,7 @@ template <int MODE>
 constexpr size_t fused_smem_bytes() {
   using real = typename Tr<MODE>::real;
   using vec = typename Tr<MODE>::vec;
-  return 3072 + PF_TILE * sizeof(vec) + max_src_tiles<MODE>() * PF_TILE * sizeof(real) +
-         (stage_positions<MODE>() ? max_src_tiles<MODE>() * PF_TILE * sizeof(vec) : 0) +
+  return 3072 + PF_TILE * sizeof(vec) + max_src_tiles<MODE>() * PF_TILE * sizeof(real) + 16 +
          (max_src_tiles<MODE>() + 1) * 24 + kSlowQ * 12 + 320 * 8;
 }
 
@@ -623,19 +650,44 @@ __device__ __forceinline__ int advance_key(const typename Tr<MODE>::real* c, int
   return gallop_key<MODE>(c, j0, n, kq);
 }
 
-// store one component of a particle's noise pair: a plain component store
-// (x and y of one particle may both take the slow path and be written by
-// different threads concurrently -- no read-modify-write of the pair)
+// store one component of a particle's scaled noise pair d(std) * d(n): a plain
+// component store (x and y of one particle may both take the slow path and be
+// written by different threads concurrently -- no read-modify-write of the pair)
 template <int MODE>
-__device__ __forceinline__ void set_comp(typename Tr<MODE>::vec& v, int comp, double x) {
+__device__ __forceinline__ void set_comp(typename Tr<MODE>::vec& v, int comp, double x, typename Tr<MODE>::vec stdv) {
   if constexpr (MODE == M_FP16) {
-    reinterpret_cast<__half*>(&v)[comp] = __double2half(x);
-  } else {
+    const __half sd = comp ? __high2half(stdv) : __low2half(stdv);
+    reinterpret_cast<__half*>(&v)[comp] = __hmul_rn(sd, __double2half(x));
+  } else if constexpr (MODE == M_FP32) {
+    const float f = __fmul_rn(comp ? stdv.y : stdv.x, __double2float_rn(x));
     if (comp)
-      v.y = (typename Tr<MODE>::real)x;
+      v.y = f;
     else
-      v.x = (typename Tr<MODE>::real)x;
+      v.x = f;
+  } else {
+    const double f = __dmul_rn(comp ? stdv.y : stdv.x, x);
+    if (comp)
+      v.y = f;
+    else
+      v.x = f;
   }
+}
+
+// d(std) * d(n) per component (the noise term of filter.py:195-202 / 362-379;
+// independent of the ancestors, so it is formed before the frame's release)
+template <int MODE>
+__device__ __forceinline__ typename Tr<MODE>::vec scale_noise(typename Tr<MODE>::vec nn, typename Tr<MODE>::vec stdv) {
+  typename Tr<MODE>::vec o;
+  if constexpr (MODE == M_FP16) {
+    o = __hmul2_rn(stdv, nn);
+  } else if constexpr (MODE == M_FP32) {
+    o.x = __fmul_rn(stdv.x, nn.x);
+    o.y = __fmul_rn(stdv.y, nn.y);
+  } else {
+    o.x = __dmul_rn(stdv.x, nn.x);
+    o.y = __dmul_rn(stdv.y, nn.y);
+  }
+  return o;
 }
 
 // canonical pairwise tree over a thread's VPT consecutive values
@@ -668,9 +720,7 @@ __global__ void __launch_bounds__(PF_TILE / (VPT * R)) pf_fused_frame(FusedArgs 
   double* s_wi = reinterpret_cast<double*>(smem + 1024);  // 2 KB
   vec* s_X = reinterpret_cast<vec*>(smem + 3072);  // per-particle noise
   real* s_c = reinterpret_cast<real*>(smem + 3072 + PF_TILE * sizeof(vec));
-  vec* s_xp = reinterpret_cast<vec*>(s_c + MS * PF_TILE);  // staged source positions (FP16)
-  unsigned char* p_tab =
-      reinterpret_cast<unsigned char*>(stage_positions<MODE>() ? (void*)(s_xp + MS * PF_TILE) : (void*)(s_c + MS * PF_TILE));
+  unsigned char* p_tab = reinterpret_cast<unsigned char*>(s_c + MS * PF_TILE);
   int* s_ts = reinterpret_cast<int*>(p_tab);                        // MS + 1 (in-track indices)
   double* s_tO = reinterpret_cast<double*>(p_tab + (MS + 1) * 8);   // MS + 1
   double* s_tM = reinterpret_cast<double*>(p_tab + (MS + 1) * 16);  // MS + 1
@@ -703,6 +753,7 @@ __global__ void __launch_bounds__(PF_TILE / (VPT * R)) pf_fused_frame(FusedArgs 
     uint4* zdst = reinterpret_cast<uint4*>(smem);
     for (int i = tid; i < 192; i += TPB) zdst[i] = zsrc[i];
   }
+  PF_TRACE(a, 0);
   if (tid == 0) s_int[3] = 0;
   // stream state at this tile's first draw, position t(2K+1) + 2*base: the
   // frame's affine jump (kernel argument) and the per-tile jump
@@ -711,14 +762,28 @@ __global__ void __launch_bounds__(PF_TILE / (VPT * R)) pf_fused_frame(FusedArgs 
   pdl_launch_dependents();
   __syncthreads();
 
+  vec drift, stdv;
+  if constexpr (MODE == M_FP16) {
+    drift = __halves2half2(__double2half(a.drift_x), __double2half(a.drift_y));
+    stdv = __halves2half2(__double2half(a.std_x), __double2half(a.std_y));
+  } else {
+    drift.x = (real)a.drift_x;
+    drift.y = (real)a.drift_y;
+    stdv.x = (real)a.std_x;
+    stdv.y = (real)a.std_y;
+  }
+
   // ---- phase 0: every draw of the tile (independent of the previous frame:
-  // overlaps the previous kernel under PDL).  Fast ziggurat path into s_X as
-  // mode-dtype noise; slow paths queued, resolved in one CTA-wide pass.
+  // overlaps the previous kernel under PDL).  Fast ziggurat path, scaled by
+  // d(std), into s_X; slow paths flagged branch-free per thread, then queued
+  // and resolved in one CTA-wide pass.
 #pragma unroll
   for (int rr = 0; rr < R; ++rr) {
     const int v = rr * TPB + tid;
     const int l0 = v * VPT;
-    unsigned long long xs = pfr::apply(pfr::Affine{a.tj[v].x, a.tj[v].y}, tstate);
+    const unsigned long long xs0 = pfr::apply(pfr::Affine{a.tj[v].x, a.tj[v].y}, tstate);
+    unsigned long long xs = xs0;
+    unsigned slow = 0;  // bit 2i+c: normal (i, c) needs the slow path
 #pragma unroll
     for (int i = 0; i < VPT; ++i) {
       double nn[2];
@@ -735,60 +800,79 @@ __global__ void __launch_bounds__(PF_TILE / (VPT * R)) pf_fused_frame(FusedArgs 
         const double x = __dmul_rn(rabs_d, s_wi[idx]);
         // sign (bit 55) flips the sign bit of the product
         nn[c] = __hiloint2double(__double2hiint(x) ^ ((whi << 8) & 0x80000000u), __double2loint(x));
-        if (((rhi << 12) | (rlo >> 20)) >= s_kihi[idx] && l0 + i < Tb) {
-          const int slot = atomicAdd(&s_int[3], 1);
-          if (slot < kSlowQ) {
-            s_qw[slot] = w;
-            s_qs[slot] = (l0 + i) * 2 + c;
-          } else {
-            nn[c] = pfr::zig_slow(w);  // queue overflow (never in practice)
-          }
-        }
+        slow |= (((rhi << 12) | (rlo >> 20)) >= s_kihi[idx] ? 1u : 0u) << (2 * i + c);
       }
-      s_X[l0 + i] = to_vec<MODE>(nn[0], nn[1]);
+      s_X[l0 + i] = scale_noise<MODE>(to_vec<MODE>(nn[0], nn[1]), stdv);
+    }
+    if (l0 + VPT > Tb) slow = l0 >= Tb ? 0u : slow & ((1u << (2 * (Tb - l0))) - 1u);
+    while (slow) {  // rare per thread: re-derive the word by stepping from xs0
+      const int bit = __ffs(slow) - 1;
+      slow &= slow - 1;
+      unsigned long long w = xs0;
+      for (int e = 0; e < bit; ++e) w = pfr::kA * w + pfr::kC;
+      const int slot = atomicAdd(&s_int[3], 1);
+      if (slot < kSlowQ) {
+        s_qw[slot] = w;
+        s_qs[slot] = (l0 + (bit >> 1)) * 2 + (bit & 1);
+      } else {
+        set_comp<MODE>(s_X[l0 + (bit >> 1)], bit & 1, pfr::zig_slow(w), stdv);  // queue overflow
+      }
     }
   }
   __syncthreads();
-  // ---- warp 0: wait for the previous kernels and find the source window
-  //      (tiles whose outputs cover this tile); other warps meanwhile resolve
-  //      the queued slow paths ---------------------------------------------
+  PF_TRACE(a, 1);
+  // ---- warp 0: wait for the previous kernels, read this tile's source window
+  //      (written by the previous frame's tile table) and start ONE bulk copy
+  //      (cp.async.bulk, mbarrier-tracked) of exactly the source tiles' local
+  //      CDFs while it fetches their table entries; the other warps meanwhile
+  //      resolve the queued slow paths ------------------------------------
+  uint64_t* s_bar = reinterpret_cast<uint64_t*>(s_misc + 200);
+  const bool bulk_ok = ((((size_t)track * K) * sizeof(real)) % 16) == 0;
   if (wid == 0 || NW == 1) {
-    pdl_wait();
-    if (a.t > 0) {
-      const int kf = base, kl = base + Tb - 1;
-      const int w0 = max(0, min(tile - 16, n - 32));
-      const int bw = min(w0 + lane, n - 1);
-      const int sv = (int)__ldg(ts + bw);
-      int res[2];
-#pragma unroll
-      for (int e = 0; e < 2; ++e) {
-        const int kk = e == 0 ? kf : kl;
-        const unsigned ball = __ballot_sync(0xffffffffu, sv <= kk);
-        const int topb = min(w0 + 31, n - 1);
-        int b = -1;
-        if (ball != 0 && (ball != 0xffffffffu || topb == n - 1)) b = min(w0 + 31 - __clz(ball), n - 1);
-        if (b < 0) {
-          int lo = 0, hi = n - 1;
-          while (lo < hi) {
-            const int mid = (lo + hi + 1) >> 1;
-            if ((int)__ldg(ts + mid) <= kk)
-              lo = mid;
-            else
-              hi = mid - 1;
-          }
-          b = lo;
-        }
-        res[e] = b;
-      }
-      const int nsrc = res[1] - res[0] + 1;
-      const int staged = nsrc <= MS ? 1 : 0;
+    if (a.t > 0) {  // acquire the previous frame's table (published before its grid ends)
       if (lane == 0) {
-        s_int[0] = res[0];
-        s_int[1] = res[1];
+        const unsigned long long* rc = a.tmax + (size_t)track * 4 + 1;
+        unsigned long long v;
+        // relaxed polling (an acquire per poll would invalidate the SM's L1
+        // under the CTAs still working on the previous frame), one acquire
+        // fence once the counter is reached
+        for (;;) {
+          asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(rc) : "memory");
+          if (v >= a.ready_target) break;
+          __nanosleep(32);
+        }
+        asm volatile("fence.acq_rel.gpu;" ::: "memory");
+      }
+      __syncwarp();
+    } else {
+      pdl_wait();  // frame 0: the likelihood maps / initial positions
+    }
+    PF_TRACE(a, 2);
+    if (a.t > 0) {
+      const int2 wn = __ldcg(reinterpret_cast<const int2*>(a.win) + (size_t)track * n + tile);
+      const int nsrc = wn.y - wn.x + 1;
+      const int staged = nsrc <= MS ? 1 : 0;
+      if (staged && bulk_ok && lane == 0) {
+        const int c0 = wn.x * PF_TILE;
+        const int cnt = min((wn.y + 1) * PF_TILE, K) - c0;
+        const uint32_t bytes = (uint32_t)((cnt * (int)sizeof(real) + 15) & ~15);  // C buffers carry 16 B of slack
+        const uint32_t bb = smem_u32(s_bar);
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bb), "r"(1) : "memory");
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bb), "r"(bytes) : "memory");
+        asm volatile(
+            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                smem_u32(s_c)),
+            "l"(Cp + c0), "r"(bytes), "r"(bb)
+            : "memory");
+      }
+      if (lane == 0) {
+        s_int[0] = wn.x;
+        s_int[1] = wn.y;
         s_int[2] = staged;
       }
       if (staged && lane <= nsrc) {
-        const int b = min(res[0] + lane, n - 1);
+        const int b = min(wn.x + lane, n - 1);
         s_ts[lane] = lane < nsrc ? (int)__ldg(ts + b) : K;
         s_tO[lane] = __ldg(tO + b);
         s_tM[lane] = __ldg(tM + b);
@@ -800,59 +884,37 @@ __global__ void __launch_bounds__(PF_TILE / (VPT * R)) pf_fused_frame(FusedArgs 
     const int nq = min(s_int[3], kSlowQ);
     for (int e = t0; e < nq; e += nt) {
       const int sl = s_qs[e];
-      set_comp<MODE>(s_X[sl >> 1], sl & 1, pfr::zig_slow(s_qw[e]));
+      set_comp<MODE>(s_X[sl >> 1], sl & 1, pfr::zig_slow(s_qw[e]), stdv);
     }
-    if (NW > 1) pdl_wait();
   }
-  const double u = a.t > 0 ? a.u_prev[track] : 0.0;
-  __syncthreads();  // window and slow-path noise visible
+  __syncthreads();  // window and slow-path noise visible (and, for every thread, the previous table)
+  PF_TRACE(a, 3);
+  const double u = a.t > 0 ? __ldcg(a.u_prev + track) : 0.0;
   int b_lo = 0, b_hi = 0, staged = 0;
   if (a.t > 0) {
     b_lo = s_int[0];
     b_hi = s_int[1];
     staged = s_int[2];
-    if (staged) {  // 16-byte copies of exactly the source tiles' local CDFs (+ positions)
-      const int c0 = b_lo * PF_TILE;
-      const int cnt = min((b_hi + 1) * PF_TILE, K) - c0;
-      constexpr int PER = 16 / sizeof(real);
-      if ((((size_t)track * K) % PER) == 0) {
-        const int nvec = cnt / PER;
-        const uint4* src = reinterpret_cast<const uint4*>(Cp + c0);
-        uint4* dst = reinterpret_cast<uint4*>(s_c);
-        for (int i = tid; i < nvec; i += TPB) dst[i] = __ldg(src + i);
-        for (int i = nvec * PER + tid; i < cnt; i += TPB) s_c[i] = Cp[c0 + i];
-      } else {
+    if (staged) {
+      if (bulk_ok) {  // wait for the bulk copy (phase 0 of the CTA's only mbarrier)
+        asm volatile(
+            "{\n\t.reg .pred p;\n\t"
+            "WAIT_%=:\n\t"
+            "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], 0;\n\t"
+            "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(s_bar))
+            : "memory");
+      } else {  // unaligned track base (odd K with several tracks): plain copy
+        const int c0 = b_lo * PF_TILE;
+        const int cnt = min((b_hi + 1) * PF_TILE, K) - c0;
         for (int i = tid; i < cnt; i += TPB) s_c[i] = Cp[c0 + i];
+        __syncthreads();
       }
-      if constexpr (stage_positions<MODE>()) {
-        constexpr int PV = 16 / sizeof(vec);
-        if ((((size_t)track * K) % PV) == 0) {
-          const int nvec = cnt / PV;
-          const uint4* src = reinterpret_cast<const uint4*>(Xp + c0);
-          uint4* dst = reinterpret_cast<uint4*>(s_xp);
-          for (int i = tid; i < nvec; i += TPB) dst[i] = __ldg(src + i);
-          for (int i = nvec * PV + tid; i < cnt; i += TPB) s_xp[i] = Xp[c0 + i];
-        } else {
-          for (int i = tid; i < cnt; i += TPB) s_xp[i] = Xp[c0 + i];
-        }
-      }
-      __syncthreads();
     }
   }
   const real* Csrc = staged ? s_c - b_lo * PF_TILE : Cp;
-  const vec* Xsrc = (stage_positions<MODE>() && staged) ? s_xp - b_lo * PF_TILE : Xp;
+  const vec* Xsrc = Xp;
   const double invK = __ddiv_rn(1.0, (double)K);
 
-  vec drift, stdv;
-  if constexpr (MODE == M_FP16) {
-    drift = __halves2half2(__double2half(a.drift_x), __double2half(a.drift_y));
-    stdv = __halves2half2(__double2half(a.std_x), __double2half(a.std_y));
-  } else {
-    drift.x = (real)a.drift_x;
-    drift.y = (real)a.drift_y;
-    stdv.x = (real)a.std_x;
-    stdv.y = (real)a.std_y;
-  }
   auto tab_s = [&](int b) -> int { return staged ? s_ts[b - b_lo] : (int)__ldg(ts + b); };
   auto tab_O = [&](int b) -> double { return staged ? s_tO[b - b_lo] : __ldg(tO + b); };
   auto tab_M = [&](int b) -> double { return staged ? s_tM[b - b_lo] : __ldg(tM + b); };
@@ -884,6 +946,7 @@ __global__ void __launch_bounds__(PF_TILE / (VPT * R)) pf_fused_frame(FusedArgs 
       // register-cached geometry of the current source tile
       int sb = tab_s(b), snext = b < b_hi ? tab_s(b + 1) : K;
       double gO = tab_O(b), gM = tab_M(b);
+      float fO = (float)gO, fM = (float)gM;  // FP16: the table holds f32 values
       int tl = b * PF_TILE, tb = min(PF_TILE, K - tl);
       const real* cb = Csrc + tl;
       int jprev = -1;
@@ -902,6 +965,8 @@ __global__ void __launch_bounds__(PF_TILE / (VPT * R)) pf_fused_frame(FusedArgs 
           sb = tab_s(b);
           gO = tab_O(b);
           gM = tab_M(b);
+          fO = (float)gO;
+          fM = (float)gM;
           tl = b * PF_TILE;
           tb = min(PF_TILE, K - tl);
           cb = Csrc + tl;
@@ -910,7 +975,7 @@ __global__ void __launch_bounds__(PF_TILE / (VPT * R)) pf_fused_frame(FusedArgs 
         typename KT::k_t kq;
         if constexpr (MODE == M_FP16) {
           // f32 tile-local point: q = ((k - s_b) + phi_b) * rho_b
-          const float qf = __fmul_rn(__fadd_rn((float)(k - sb), (float)gO), (float)gM);
+          const float qf = __fmul_rn(__fadd_rn((float)(k - sb), fO), fM);
           kq = __half_as_ushort(__float2half_ru(fminf(fmaxf(qf, 0.0f), 1.0f)));
         } else {
           const double p = point_of<MODE>(k, u, K, invK);
@@ -928,24 +993,53 @@ __global__ void __launch_bounds__(PF_TILE / (VPT * R)) pf_fused_frame(FusedArgs 
       for (int i = 0; i < VPT; ++i)
         if (l0 + i < Tb) a.dbg_anc[(size_t)track * K + base + l0 + i] = anc[i];
     }
+    // all VPT ancestor gathers first (independent, read-only X_prev), then
+    // propagation and all VPT map lookups, then the new positions' stores --
+    // no store sits between loads, so nothing serialises the memory latency
+    vec xa[VPT];
+#pragma unroll
+    for (int i = 0; i < VPT; ++i) {
+      if (l0 + i < Tb) {
+        xa[i] = __ldg(Xsrc + anc[i]);
+      } else {
+        xa[i].x = (real)0;
+        xa[i].y = (real)0;
+      }
+    }
 #pragma unroll
     for (int i = 0; i < VPT; ++i) {
       const int l = l0 + i;
       if (l < Tb) {
-        const vec xn = prop<MODE>(Xsrc[anc[i]], s_X[l], drift, stdv);
-        Xn[base + l] = xn;
+        const vec xn = prop<MODE>(xa[i], s_X[l], drift);
         const int ix = round_clamp<MODE>(xn.x, -a.r, a.W - 1 + a.r);
         const int iy = round_clamp<MODE>(xn.y, -a.r, a.H - 1 + a.r);
-        const real L = map[(iy + a.r) * a.Wm + (ix + a.r)];
-        Lr[rr][i] = L;
+        Lr[rr][i] = __ldg(map + (iy + a.r) * a.Wm + (ix + a.r));
         Xr[rr][i] = xn;
-        if (gt_real<MODE>(L, tmax)) tmax = L;
       } else {
         Lr[rr][i] = neg_inf<MODE>();
         Xr[rr][i].x = (real)0;
         Xr[rr][i].y = (real)0;
       }
     }
+    {
+      constexpr int VB = VPT * (int)sizeof(vec);
+      if (VB % 16 == 0 && l0 + VPT <= Tb && ((((size_t)track * K) * sizeof(vec)) % 16) == 0) {
+        uint4* dst = reinterpret_cast<uint4*>(Xn + base + l0);
+#pragma unroll
+        for (int q = 0; q < VB / 16; ++q) {
+          uint4 o;
+          memcpy(&o, reinterpret_cast<const unsigned char*>(&Xr[rr][0]) + 16 * q, 16);
+          dst[q] = o;
+        }
+      } else {
+#pragma unroll
+        for (int i = 0; i < VPT; ++i)
+          if (l0 + i < Tb) Xn[base + l0 + i] = Xr[rr][i];
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < VPT; ++i)
+      if (gt_real<MODE>(Lr[rr][i], tmax)) tmax = Lr[rr][i];
   }
   if (a.dbg_anc != nullptr) {  // debug capture (parity tests): recompute-free copies
 #pragma unroll
@@ -956,6 +1050,7 @@ __global__ void __launch_bounds__(PF_TILE / (VPT * R)) pf_fused_frame(FusedArgs 
         if (l0 + i < Tb) reinterpret_cast<real*>(a.dbg_L)[(size_t)track * K + base + l0 + i] = Lr[rr][i];
     }
   }
+  PF_TRACE(a, 4);
   // tile max (exact): warp max, one barrier, every thread reduces the NW values
 #pragma unroll
   for (int d = 16; d >= 1; d >>= 1) {
@@ -1100,6 +1195,7 @@ __global__ void __launch_bounds__(PF_TILE / (VPT * R)) pf_fused_frame(FusedArgs 
   if (tid == 0) {
     const size_t ri = (size_t)track * n + tile;
     a.rec_m[ri] = to_d(mtile);
+    atomicMax(a.tmax + (size_t)track * 4, okey(to_d(mtile)));  // the table reads the track max directly
     a.rec_S[ri] = (long long)S;
     if constexpr (MODE == M_FP16) {
       long long sx = 0, sy = 0;
@@ -1125,6 +1221,10 @@ __global__ void __launch_bounds__(PF_TILE / (VPT * R)) pf_fused_frame(FusedArgs 
       a.rec_Y[ri] = __double_as_longlong(by[0]);
     }
   }
+  PF_TRACE(a, 5);
+  // complete only after the previous grid (keeps grid completion in stream
+  // order: the next table reuses the exchange counters and records)
+  if (a.t > 0 && tid == 0) pdl_wait();
 }
 
 // ------------------------------------------------------------------------
@@ -1153,6 +1253,8 @@ struct TableArgs {
   unsigned long long* sync;     // per track: [0] max key, [1] arrivals (max), [2] arrivals (sums), [3] ticket
   long long* agg;               // per track x chunk: chunk mass total
   double* roots;                // per track x chunk x 3: estimate subtree roots
+  unsigned long long* trace;    // optional: [chunk][8] %globaltimer stamps (track 0)
+  int2* win;                    // [track][tile]: source window of each destination tile (next frame)
 };
 
 // canonical pairwise accumulation over a power-of-two run (binary counter)
@@ -1177,15 +1279,6 @@ struct PwAcc {
   }
 };
 
-// order-preserving map double -> uint64 (for atomicMax); 0 is below every key
-__device__ __forceinline__ unsigned long long okey(double d) {
-  const unsigned long long b = (unsigned long long)__double_as_longlong(d);
-  return (b & 0x8000000000000000ULL) ? ~b : (b | 0x8000000000000000ULL);
-}
-__device__ __forceinline__ double okey_inv(unsigned long long k) {
-  const unsigned long long b = (k & 0x8000000000000000ULL) ? (k & 0x7fffffffffffffffULL) : ~k;
-  return __longlong_as_double((long long)b);
-}
 __device__ __forceinline__ void spin_until(unsigned long long* ctr, unsigned long long target) {
   while (atomicAdd(ctr, 0ULL) < target) __nanosleep(64);
 }
@@ -1201,6 +1294,7 @@ template <int MODE>
 __global__ void __launch_bounds__(1024) pf_tile_table(TableArgs a) {
   __shared__ long long s_i[32];
   __shared__ double s_d[3 * 32 + 4];
+  __shared__ long long s_sb[1024];
   __shared__ int s_last;
   constexpr int FB = Tr<MODE>::FB;
   const int chunk = blockIdx.x, track = blockIdx.y, tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
@@ -1210,34 +1304,20 @@ __global__ void __launch_bounds__(1024) pf_tile_table(TableArgs a) {
   const bool valid = b < n;
   unsigned long long* sy = a.sync + (size_t)track * 4;
 
+  PF_TRACE(a, 0);
   pdl_launch_dependents();
   // the frame's resampling uniform: stream position t(2K+1)+2K
   const double u = pfr::uniform_of(a.ua * a.x0[track] + a.uc);
   pdl_wait();  // tile records of this frame's fused kernel
+  PF_TRACE(a, 1);
   const size_t rb = (size_t)track * n + (valid ? b : 0);
   const double m1 = valid ? a.rec_m[rb] : __longlong_as_double(0xfff0000000000000LL);
   const long long S1 = valid ? a.rec_S[rb] : 0, X1 = valid ? a.rec_X[rb] : 0, Y1 = valid ? a.rec_Y[rb] : 0;
 
-  // 1. global max (exact)
-  double m = m1;
-#pragma unroll
-  for (int d = 16; d >= 1; d >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, d));
-  if (lane == 0) s_d[wid] = m;
-  __syncthreads();
-  if (tid == 0) {
-    double mm = s_d[0];
-    for (int w = 1; w < nw; ++w) mm = fmax(mm, s_d[w]);
-    if (nc > 1) {
-      atomicMax(sy + 0, okey(mm));
-      __threadfence();
-      atomicAdd(sy + 1, 1ULL);
-      spin_until(sy + 1, (unsigned long long)nc);
-      mm = okey_inv(atomicAdd(sy + 0, 0ULL));
-    }
-    s_d[96] = mm;
-  }
-  __syncthreads();
-  m = s_d[96];
+  // 1. global max (exact): the fused kernel's CTAs atomicMax'ed their tile
+  //    maxima into sy[0] (order keys); reset by the last reader below
+  const double m = okey_inv(__ldcg(sy + 0));
+  PF_TRACE(a, 4);
   const double scale = ldexp(1.0, a.Q - FB);
   const double Kd = __ll2double_rn(a.K);
   const double invK = __ddiv_rn(1.0, Kd);
@@ -1259,6 +1339,7 @@ __global__ void __launch_bounds__(1024) pf_tile_table(TableArgs a) {
       __threadfence();
       atomicAdd(sy + 2, 1ULL);
       spin_until(sy + 2, (unsigned long long)nc);
+      if (chunk == 0) sy[0] = 0;  // every chunk read the max key before arriving
     }
     __syncthreads();
     long long before = 0, all = 0;
@@ -1302,6 +1383,7 @@ __global__ void __launch_bounds__(1024) pf_tile_table(TableArgs a) {
       sb = k;
     }
     a.tab_s[rb] = sb;
+    s_sb[tid] = sb;
     if constexpr (MODE == M_FP16) {
       // f32 tile-local coordinate q = ((k - s_b) + phi_b) * rho_b
       a.tab_O[rb] = (double)__double2float_rn(__dsub_rn(__dadd_rn((double)sb, u), __dmul_rn(Kd, O)));
@@ -1322,6 +1404,46 @@ __global__ void __launch_bounds__(1024) pf_tile_table(TableArgs a) {
     vy = __dmul_rn(f, Y);
     vd = __dmul_rn(f, (double)S1);
   }
+  // source windows of the next frame: destination tile d starts (ends) in
+  // source tile b iff its first (last) output index lies in [s_b, s_{b+1});
+  // the ranges partition [0, K), so every d is written exactly once
+  __syncthreads();
+  if (valid) {
+    const long long sb = s_sb[tid];
+    long long sn;
+    if (b + 1 >= n) {
+      sn = a.K;
+    } else if (tid + 1 < TPB) {
+      sn = s_sb[tid + 1];
+    } else {  // first tile of the next chunk: same formula on its exact prefix
+      const double On = __ddiv_rn((double)(excl + mass), Sq);
+      long long k = (long long)floor(__dsub_rn(__dmul_rn(On, Kd), u));
+      k = min(max(k, 0LL), a.K);
+      while (k > 0 && point_of<MODE>(k - 1, u, a.K, invK) > On) --k;
+      while (k < a.K && point_of<MODE>(k, u, a.K, invK) <= On) ++k;
+      sn = k;
+    }
+    const long long K = a.K;
+    auto first_lo = [&](long long x) -> long long { return min((long long)n, (x + PF_TILE - 1) / PF_TILE); };
+    auto first_hi = [&](long long x) -> long long {
+      return x >= K ? (long long)n : min((long long)n - 1, max(0LL, (x - (PF_TILE - 1) + PF_TILE - 1) / PF_TILE));
+    };
+    int2* wt = a.win + (size_t)track * n;
+    for (long long d = first_lo(sb), e = first_lo(sn); d < e; ++d) wt[d].x = b;
+    for (long long d = first_hi(sb), e = first_hi(sn); d < e; ++d) wt[d].y = b;
+  }
+  // early release of the next frame: table entries, windows and u are
+  // published with a per-track monotone counter (sy[1], +1 per chunk); the
+  // next fused kernel acquires it instead of waiting for this grid to end
+  // (the estimate below is off the critical path)
+  if (chunk == 0 && tid == 0) {
+    a.u_out[track] = u;
+    if (nc == 1) sy[0] = 0;  // all threads read the max key before the barrier above
+  }
+  __threadfence();
+  __syncthreads();
+  if (tid == 0) atomicAdd(sy + 1, 1ULL);
+  PF_TRACE(a, 5);
   // canonical pairwise tree: lanes, warps (zero padded), chunks (last CTA)
 #pragma unroll
   for (int d = 1; d < 32; d <<= 1) {
@@ -1358,6 +1480,7 @@ __global__ void __launch_bounds__(1024) pf_tile_table(TableArgs a) {
     }
   }
   __syncthreads();
+  PF_TRACE(a, 2);
   if (!s_last) return;
   if (nc > 1) {  // last CTA: tree over the chunk roots (power-of-two padded)
     __threadfence();
@@ -1417,15 +1540,16 @@ __global__ void __launch_bounds__(1024) pf_tile_table(TableArgs a) {
     double* tr = a.traj + ((size_t)track * a.traj_stride + a.traj_index) * 2;
     tr[0] = ex;
     tr[1] = ey;
-    a.u_out[track] = u;
+    PF_TRACE(a, 3);
     if (!(vd > 0.0) || !isfinite(vd) || !isfinite(ex) || !isfinite(ey)) atomicMin(a.degenerate + track, a.t);
-    if (nc > 1) {  // every CTA has passed both exchanges: reset for the next frame
-      sy[0] = 0;
-      sy[1] = 0;
+    // every CTA of the track has passed the exchanges: reset them for the
+    // next frame's table (which starts only after the next fused kernel
+    // completes, and that ends with griddepcontrol.wait on this grid)
+    if (nc > 1) {
       sy[2] = 0;
       sy[3] = 0;
-      __threadfence();
     }
+    __threadfence();
   }
 }
 
