@@ -48,6 +48,9 @@ CONFIGS = {
                desc="C3: 1024x1024 video, 100 frames, 16M particles, FP16 half2"),
     "c4": dict(W=128, H=128, F=100, K=65536, precision="fp16", tracks=8192, videos=8,
                desc="C4: 8192 independent 128x128 tracks x 64K particles, FP16 (tracks split over GPUs)"),
+    "c5": dict(W=1024, H=1024, F=10, K=1 << 30, precision="fp16", tracks=1, videos=1, sharded=True,
+               desc="C5: one 2^30-particle FP16 filter, 1024x1024 video, 10 frames, particle range sharded "
+                    "over the GPUs (NCCL all-gathers of shard max / sums, peer reads of remote ancestors)"),
 }
 
 
@@ -243,6 +246,65 @@ def _config_block(cfg, args):
 # ---------------------------------------------------------------------------
 
 
+def run_sharded(args, cfg, rank, world, local, dist, dev_frames, host_frames, truth, flush):
+    """C5: one filter, particle range sharded over the ranks (strong scaling)."""
+    import torch
+
+    import paper_2308_00763_b200 as pf
+    from paper_2308_00763_b200.sharded import DistShard
+    from paper_2308_00763_b200.sharding import max_over_ranks
+
+    F, K, W, H, prec = cfg["F"], cfg["K"], cfg["W"], cfg["H"], cfg["precision"]
+    sh = DistShard(K, prec, W, H, 42, tpb=args.tpb or None, device=local)
+    stream = sh.stream
+
+    def steps(n, frames):
+        tot = 0.0
+        for _ in range(n):
+            flush.zero_()
+            torch.cuda.synchronize()
+            dist.barrier()
+            sh.reset()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            traj = sh.run(frames)
+            e1.record(stream)
+            e1.synchronize()
+            tot += e0.elapsed_time(e1)
+        return tot, traj
+
+    steps(args.warmup, dev_frames)
+    clocks = ClockSampler(local)
+    clocks.start()
+    dev_ms, traj = steps(args.steps, dev_frames)
+    clk = clocks.stop()
+    dev_ms = max_over_ranks(dev_ms, dist, device="cuda")
+    value = K * F * args.steps / (dev_ms * 1e-3)
+    rmse, mean_err, max_err = pf.accuracy_metrics(traj, truth)
+    e2e_ms, _ = steps(args.steps, host_frames)  # frames H2D + trajectory D2H inside the events
+    e2e_s = max_over_ranks(e2e_ms, dist, device="cuda") * 1e-3
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": dev_ms / args.steps, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": DTYPE_TAG[prec], "data": "synthetic",
+            "config": dict(_config_block(cfg, args), parallelism=(
+                f"one filter, particle range over {world} GPUs: 3 all-gathers (8 B, 32 B, 4 B per rank) "
+                f"per frame on the library stream (NCCL), remote ancestors read over CUDA-IPC peer mappings")),
+            "e2e": {"value": K * F * args.steps / e2e_s, "unit": UNIT, "h2d_bytes_per_step": int(host_frames.nbytes),
+                    "d2h_bytes_per_step": int(F * 2 * 8),
+                    "timer": "CUDA events on the library stream around run(host frames), max over ranks"},
+            "roofline": None, "cpu_baseline": None, "clocks": clk,
+            "gpu_launches": (4 * F + 1) * args.steps,
+            "tracking": {"rmse_px": rmse, "mean_err_px": mean_err, "max_err_px": max_err},
+        }
+        print(json.dumps(line), flush=True)
+    sh.close()
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -324,6 +386,9 @@ def main():
         return max_over_ranks(x, dist, device="cuda")
 
     prec = cfg["precision"]
+    if cfg.get("sharded") and world > 1:
+        run_sharded(args, cfg, rank, world, local, dist, dev_frames, host_frames, truths[0], flush)
+        return
     f = make(prec)
     if args.profile_only:
         f.run_frames(dev_frames, F)

@@ -101,6 +101,47 @@ int pf_last_timings(const pf_handle* h, float* ms6);
  * (events between launches on the handle's stream). */
 int pf_set_profiling(pf_handle* h, int32_t on);
 
+/* ---------------------------------------------------------------------------
+ * Sharded filter (one track, particle range split over n_shards <= 8 GPUs or
+ * handles).  Replaces, for a filter too large for one
+ * device, the reference's single-process run() loop (filter.py:591-662): the
+ * resampling CDF / normalisation become per-shard exact partial sums combined
+ * by three small all-gathers per frame, and resampled ancestors on other
+ * shards are read peer-to-peer (NVLink) through the peer buffers below.
+ * Results are bit-identical to the same filter run by pf_create/pf_run.
+ *
+ * Tiles per shard = next power of two >= ceil(n_tiles / n_shards); shard r
+ * holds global tiles [r * shard_tiles, ...) (pf_shard_info).  Per frame f,
+ * on every shard's stream, in this order:
+ *   pf_shard_fused(h, f)
+ *   all-gather 8 B:   exchange[0] (send) -> exchange[1] (recv, [n_shards])
+ *   pf_shard_tables(h)
+ *   all-gather 32 B:  exchange[2] (send) -> exchange[3] (recv, [n_shards][4])
+ *   pf_shard_finish(h, f)
+ *   barrier (every shard's window records written before the next frame)
+ * between pf_shard_begin (frames upload + likelihood maps) and pf_shard_end
+ * (trajectory download, PF_EDEGENERATE check).  Shards in one process use
+ * pf_shard_local_allgather(hs, S, 0 | 1 | 2) for the three exchanges. */
+int pf_shard_create(pf_handle** out, const pf_config* cfg, int32_t n_shards, int32_t shard);
+/* {shard_tiles, first global tile, local tiles, local particles} */
+int pf_shard_info(const pf_handle* h, int64_t* out4);
+/* device pointers a peer needs: X0, X1, C0, C1, tab_s, tab_O, tab_invM, win */
+int pf_shard_buffers(pf_handle* h, void** out8);
+/* the same eight buffers as cudaIpcMemHandle_t[8] (8 x 64 bytes) */
+int pf_shard_ipc_export(pf_handle* h, void* out512);
+/* peer buffers: raw device pointers (same process / already mapped) or IPC handles */
+int pf_shard_set_peer(pf_handle* h, int32_t peer, void* const* ptrs8);
+int pf_shard_open_peer(pf_handle* h, int32_t peer, const void* handles512);
+/* exchange buffers (device): {max key u64 send, u64[n_shards] recv, i64[4] send, i64[n_shards][4] recv} */
+int pf_shard_exchange(pf_handle* h, void** out4);
+void* pf_shard_stream(pf_handle* h);
+int pf_shard_begin(pf_handle* h, const uint8_t* frames, int32_t n_frames, int32_t frames_on_device);
+int pf_shard_fused(pf_handle* h, int32_t frame);
+int pf_shard_tables(pf_handle* h);
+int pf_shard_finish(pf_handle* h, int32_t frame);
+int pf_shard_end(pf_handle* h, int32_t n_frames, double* traj_out);
+int pf_shard_local_allgather(pf_handle* const* handles, int32_t n_shards, int32_t which);
+
 /* Timeline tracing (performance analysis): when on, thread 0 of every CTA of
  * track 0 stamps %globaltimer (ns) at fixed points of the next runs:
  * per frame f, (n_tiles + n_chunks) records of 8 uint64 -- fused tile b:

@@ -66,6 +66,20 @@ SIGNATURES = [
     ("pf_last_timings", C.c_int, [_VP, C.POINTER(C.c_float)]),
     ("pf_last_launches", C.c_int64, [_VP]),
     ("pf_set_trace", C.c_int, [_VP, C.c_int32]),
+    ("pf_shard_create", C.c_int, [C.POINTER(_VP), C.POINTER(pf_config), C.c_int32, C.c_int32]),
+    ("pf_shard_info", C.c_int, [_VP, _VP]),
+    ("pf_shard_buffers", C.c_int, [_VP, _VP]),
+    ("pf_shard_ipc_export", C.c_int, [_VP, _VP]),
+    ("pf_shard_set_peer", C.c_int, [_VP, C.c_int32, _VP]),
+    ("pf_shard_open_peer", C.c_int, [_VP, C.c_int32, _VP]),
+    ("pf_shard_exchange", C.c_int, [_VP, _VP]),
+    ("pf_shard_stream", C.c_void_p, [_VP]),
+    ("pf_shard_begin", C.c_int, [_VP, _VP, C.c_int32, C.c_int32]),
+    ("pf_shard_fused", C.c_int, [_VP, C.c_int32]),
+    ("pf_shard_tables", C.c_int, [_VP]),
+    ("pf_shard_finish", C.c_int, [_VP, C.c_int32]),
+    ("pf_shard_end", C.c_int, [_VP, C.c_int32, _VP]),
+    ("pf_shard_local_allgather", C.c_int, [_VP, C.c_int32, C.c_int32]),
     ("pf_get_trace", C.c_int, [_VP, _VP, C.c_int64]),
     ("pf_get_state", C.c_int, [_VP, C.c_int32, _VP, _VP, _VP]),
     ("pf_get_debug", C.c_int, [_VP, C.c_int32, _VP, _VP]),

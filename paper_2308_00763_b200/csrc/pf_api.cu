@@ -190,6 +190,17 @@ struct pf_handle {
   int g_cur = -1, g_F = -1;
   const void* g_maps = nullptr;
   const void* g_traj = nullptr;
+  // sharding (pf_shard_*): this handle holds global tiles [tile0, tile0 + nl)
+  long long Kl = 0;  // particles per track held here (== K unless sharded)
+  int nl = 0;        // tiles per track held here (== n_tiles unless sharded)
+  int tile0 = 0, n_shards = 1, shard = 0, shard_tiles = 0, sh_chunks = 0;
+  void* peer[PF_MAX_SHARDS][8] = {};  // per shard: X0, X1, C0, C1, tab_s, tab_O, tab_invM, win
+  bool peer_ipc[PF_MAX_SHARDS] = {};
+  long long *sh_mass = nullptr, *sh_ctot = nullptr, *sh_send = nullptr, *sh_gsum = nullptr;
+  double* sh_croots = nullptr;
+  unsigned long long* sh_gmax = nullptr;
+  cudaEvent_t xev = nullptr;
+  int sh_F = 0;
   unsigned long long* d_trace = nullptr;  // pf_set_trace: [frame][n_tiles + n_chunks][8]
   size_t trace_cap = 0;
   bool tracing = false;
@@ -281,6 +292,14 @@ int pf_destroy(pf_handle* h) {
                   h->d_maps, h->d_traj, h->d_degen, h->dbg_anc, h->dbg_L, h->d_trace};
   for (void* p : ptrs)
     if (p) cudaFree(p);
+  void* sptrs[] = {h->sh_mass, h->sh_ctot, h->sh_croots, h->sh_send, h->sh_gsum, h->sh_gmax};
+  for (void* p : sptrs)
+    if (p) cudaFree(p);
+  for (int sh = 0; sh < PF_MAX_SHARDS; ++sh)
+    if (h->peer_ipc[sh])
+      for (int i = 0; i < 8; ++i)
+        if (h->peer[sh][i]) cudaIpcCloseMemHandle(h->peer[sh][i]);
+  if (h->xev) cudaEventDestroy(h->xev);
   for (auto& e : h->ev)
     if (e) cudaEventDestroy(e);
   for (auto& e : h->pev) cudaEventDestroy(e);
@@ -324,11 +343,16 @@ static int validate(const pf_config* c, std::string& err) {
   return PF_OK;
 }
 
-int pf_create(pf_handle** out, const pf_config* cfg) {
+static int create_impl(pf_handle** out, const pf_config* cfg, int n_shards, int shard) {
   if (!out) return PF_EINVAL;
   *out = nullptr;
   int rc = validate(cfg, g_err);
   if (rc) return rc;
+  if (n_shards < 1 || n_shards > PF_MAX_SHARDS || shard < 0 || shard >= n_shards ||
+      (n_shards > 1 && cfg->n_tracks != 1)) {
+    g_err = "bad shard layout (1..8 shards of one track)";
+    return PF_EINVAL;
+  }
   pf_handle* h = new pf_handle();
   h->precision = cfg->precision;
   h->km = kmode_of(cfg->precision);
@@ -358,6 +382,26 @@ int pf_create(pf_handle** out, const pf_config* cfg) {
   h->rs = real_size(h->km);
   h->vs = 2 * h->rs;
   h->n_tiles = (int)((h->K + PF_TILE - 1) / PF_TILE);
+  h->n_shards = n_shards;
+  h->shard = shard;
+  if (n_shards > 1) {
+    // power-of-two tiles per shard: every shard's estimate subtree is a node
+    // of the single-GPU canonical tree (bit-identical results)
+    h->shard_tiles = next_pow2((h->n_tiles + n_shards - 1) / n_shards);
+    if ((long long)(n_shards - 1) * h->shard_tiles >= h->n_tiles) {
+      g_err = "too few tiles for this many shards (every shard must hold particles)";
+      delete h;
+      return PF_EINVAL;
+    }
+    h->tile0 = shard * h->shard_tiles;
+    h->nl = std::min(h->n_tiles - h->tile0, h->shard_tiles);
+    h->Kl = std::min(h->K, (long long)(h->tile0 + h->nl) * PF_TILE) - (long long)h->tile0 * PF_TILE;
+    h->sh_chunks = (h->nl + pfk::kShardChunk - 1) / pfk::kShardChunk;
+  } else {
+    h->shard_tiles = h->n_tiles;
+    h->nl = h->n_tiles;
+    h->Kl = h->K;
+  }
   h->n_pad = next_pow2(h->n_tiles);
   int lg = 0;
   while ((1LL << lg) < h->n_tiles) ++lg;
@@ -387,8 +431,8 @@ int pf_create(pf_handle** out, const pf_config* cfg) {
   CK(init_device_tables(h->device, e));
   CK(cudack(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking), "stream"));
   for (auto& ev : h->ev) CK(cudack(cudaEventCreate(&ev), "event"));
-  const size_t KT = (size_t)h->K * h->n_tracks;
-  const size_t NT = (size_t)h->n_tiles * h->n_tracks;
+  const size_t KT = (size_t)h->Kl * h->n_tracks;
+  const size_t NT = (size_t)h->nl * h->n_tracks;
   for (int i = 0; i < 2; ++i) {
     CK(cudack(cudaMalloc(&h->X[i], KT * h->vs), "X"));
     CK(cudack(cudaMalloc(&h->C[i], KT * h->rs + 16), "C"));  // slack: 16-byte rounded bulk copies
@@ -423,15 +467,15 @@ int pf_create(pf_handle** out, const pf_config* cfg) {
   CK(cudack(cudaMemcpy(h->tj, tj.data(), nv * sizeof(ulonglong2), cudaMemcpyHostToDevice), "tj"));
   // per-tile jumps f^(2 * tile * PF_TILE) and f^(2K)
   {
-    std::vector<ulonglong2> tt(h->n_tiles);
+    std::vector<ulonglong2> tt(h->nl);  // local tile b is global tile tile0 + b
     const pfr::Affine step = pfr::affine_pow(2ULL * PF_TILE);
-    pfr::Affine f{1, 0};
-    for (int b = 0; b < h->n_tiles; ++b) {
+    pfr::Affine f = pfr::affine_pow(2ULL * PF_TILE * (unsigned long long)h->tile0);
+    for (int b = 0; b < h->nl; ++b) {
       tt[b] = make_ulonglong2(f.a, f.c);
       f = pfr::compose(step, f);
     }
-    CK(cudack(cudaMalloc(&h->tt, h->n_tiles * sizeof(ulonglong2)), "tt"));
-    CK(cudack(cudaMemcpy(h->tt, tt.data(), h->n_tiles * sizeof(ulonglong2), cudaMemcpyHostToDevice), "tt"));
+    CK(cudack(cudaMalloc(&h->tt, h->nl * sizeof(ulonglong2)), "tt"));
+    CK(cudack(cudaMemcpy(h->tt, tt.data(), h->nl * sizeof(ulonglong2), cudaMemcpyHostToDevice), "tt"));
   }
   // exp16 table
   std::vector<uint16_t> ex(65536);
@@ -483,11 +527,25 @@ int pf_create(pf_handle** out, const pf_config* cfg) {
       ce = cudaFuncSetAttribute(pfk::pf_map_half, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->map_smem);
     CK(cudack(ce, "map smem attr"));
   }
+  if (n_shards > 1) {
+    CK(cudack(cudaMalloc(&h->sh_mass, (size_t)h->nl * 8), "shard"));
+    CK(cudack(cudaMalloc(&h->sh_ctot, (size_t)h->sh_chunks * 8), "shard"));
+    CK(cudack(cudaMalloc(&h->sh_croots, (size_t)h->sh_chunks * 3 * 8), "shard"));
+    CK(cudack(cudaMalloc(&h->sh_send, 4 * 8), "shard"));
+    CK(cudack(cudaMalloc(&h->sh_gsum, (size_t)n_shards * 4 * 8), "shard"));
+    CK(cudack(cudaMalloc(&h->sh_gmax, (size_t)n_shards * 8), "shard"));
+    CK(cudack(cudaEventCreateWithFlags(&h->xev, cudaEventDisableTiming), "event"));
+  }
+  // own buffers as shard `shard`'s source pointers (peers are set later)
+  void* own[8] = {h->X[0], h->X[1], h->C[0], h->C[1], h->tab_s, h->tab_O, h->tab_invM, h->win};
+  for (int i = 0; i < 8; ++i) h->peer[shard][i] = own[i];
   CK(pf_reset(h, cfg->start_x, cfg->start_y));
 #undef CK
   *out = h;
   return PF_OK;
 }
+
+int pf_create(pf_handle** out, const pf_config* cfg) { return create_impl(out, cfg, 1, 0); }
 
 int pf_reset(pf_handle* h, double x0, double y0) {
   if (!h) return PF_EINVAL;
@@ -497,7 +555,7 @@ int pf_reset(pf_handle* h, double x0, double y0) {
   h->cur = 0;
   h->frame_counter = 0;
   h->degenerate_frame = -1;
-  const long long n = h->K * h->n_tracks;
+  const long long n = h->Kl * h->n_tracks;
   const int tb = 256;
   const unsigned nb = (unsigned)((n + tb - 1) / tb);
   if (h->km == 0)
@@ -556,18 +614,25 @@ static int launch_frame(pf_handle* h, const void* map_slot, long long map_video_
   pfk::FusedArgs a{};
   a.K = h->K;
   a.n_tiles = h->n_tiles;
+  a.K_local = h->Kl;
+  a.n_local = h->nl;
+  a.tile0 = h->tile0;
+  a.src.n_shards = h->n_shards;
+  a.src.shard_tiles = h->shard_tiles;
+  for (int sh = 0; sh < h->n_shards; ++sh) {
+    a.src.X[sh] = h->peer[sh][h->cur];
+    a.src.C[sh] = h->peer[sh][2 + h->cur];
+    a.src.ts[sh] = (const long long*)h->peer[sh][4];
+    a.src.tO[sh] = (const double*)h->peer[sh][5];
+    a.src.tM[sh] = (const double*)h->peer[sh][6];
+  }
   a.H = h->H;
   a.W = h->W;
   a.r = h->r;
   a.Wm = h->Wm;
   a.t = (int)h->frame_counter;
-  a.X_prev = h->X[h->cur];
   a.X_new = h->X[1 - h->cur];
-  a.C_prev = h->C[h->cur];
   a.C_new = h->C[1 - h->cur];
-  a.tab_s = h->tab_s;
-  a.tab_O = h->tab_O;
-  a.tab_invM = h->tab_invM;
   a.u_prev = h->u;
   a.map = map_slot;
   a.map_video_stride = map_video_stride;
@@ -592,12 +657,17 @@ static int launch_frame(pf_handle* h, const void* map_slot, long long map_video_
   a.tt = h->tt;
   a.win = h->win;
   a.tmax = h->tsync;
-  a.ready_target = (unsigned long long)h->n_chunks * (unsigned long long)h->frame_counter;
+  // sharded frames are stream-ordered (collectives in between): no early release
+  a.ready_target = h->n_shards > 1 ? 0ULL : (unsigned long long)h->n_chunks * (unsigned long long)h->frame_counter;
   const size_t tr_frame = (size_t)(h->n_tiles + h->n_chunks) * 8;
-  a.trace = h->tracing ? h->d_trace + (size_t)traj_index * tr_frame : nullptr;
-  PF_CUDA(launch_pdl(h, (const void*)fused_kernel(h), dim3(h->n_tiles, h->n_tracks), dim3(h->tpb), h->fused_smem, a),
+  a.trace = (h->tracing && h->d_trace) ? h->d_trace + (size_t)traj_index * tr_frame : nullptr;
+  PF_CUDA(launch_pdl(h, (const void*)fused_kernel(h), dim3(h->nl, h->n_tracks), dim3(h->tpb), h->fused_smem, a),
           h->err);
   PF_CUDA(cudaGetLastError(), h->err);
+  if (h->n_shards > 1) {  // the sharded tables run after the host's collectives (pf_shard_*)
+    h->launches += 1;
+    return PF_OK;
+  }
   if (h->profiling) PF_CUDA(cudaEventRecord(h->pev[3 * traj_index + 1], h->stream), h->err);
   pfk::TableArgs t{};
   t.K = h->K;
@@ -629,7 +699,7 @@ static int launch_frame(pf_handle* h, const void* map_slot, long long map_video_
   t.agg = h->tagg;
   t.roots = h->troots;
   t.win = h->win;
-  t.trace = h->tracing ? h->d_trace + (size_t)traj_index * tr_frame + (size_t)h->n_tiles * 8 : nullptr;
+  t.trace = (h->tracing && h->d_trace) ? h->d_trace + (size_t)traj_index * tr_frame + (size_t)h->n_tiles * 8 : nullptr;
   PF_CUDA(launch_pdl(h, tk, dim3(h->n_chunks, h->n_tracks), dim3(h->tpb_table), 0, t), h->err);
   PF_CUDA(cudaGetLastError(), h->err);
   if (h->profiling) PF_CUDA(cudaEventRecord(h->pev[3 * traj_index + 2], h->stream), h->err);
@@ -654,6 +724,10 @@ static int finish_degenerate(pf_handle* h) {
 
 int pf_run(pf_handle* h, const uint8_t* frames, int32_t F, int32_t on_device, double* traj_out) {
   if (!h || !frames || F < 1 || !traj_out) return PF_EINVAL;
+  if (h->n_shards > 1) {
+    h->err = "sharded handle: drive frames with pf_shard_*";
+    return PF_EINVAL;
+  }
   PF_CUDA(cudaSetDevice(h->device), h->err);
   h->launches = 0;
   const size_t fbytes = (size_t)h->n_videos * F * h->H * h->W;
@@ -793,7 +867,7 @@ int pf_get_state(pf_handle* h, int32_t track, void* xs, void* ys, void* cdf) {
   if (!h || track < 0 || track >= h->n_tracks) return PF_EINVAL;
   PF_CUDA(cudaSetDevice(h->device), h->err);
   PF_CUDA(cudaStreamSynchronize(h->stream), h->err);
-  const size_t K = (size_t)h->K;
+  const size_t K = (size_t)h->Kl;
   std::vector<unsigned char> buf(K * h->vs);
   PF_CUDA(cudaMemcpy(buf.data(), (char*)h->X[h->cur] + track * K * h->vs, K * h->vs, cudaMemcpyDeviceToHost), h->err);
   for (size_t k = 0; k < K; ++k) {
@@ -808,7 +882,7 @@ int pf_get_state(pf_handle* h, int32_t track, void* xs, void* ys, void* cdf) {
 int pf_get_debug(pf_handle* h, int32_t track, int64_t* anc, void* loglik) {
   if (!h || track < 0 || track >= h->n_tracks) return PF_EINVAL;
   PF_CUDA(cudaSetDevice(h->device), h->err);
-  const size_t K = (size_t)h->K, KT = K * h->n_tracks;
+  const size_t K = (size_t)h->Kl, KT = K * h->n_tracks;
   if (!h->dbg_anc) {
     // enable debug capture for subsequent frames
     PF_CUDA(cudaMalloc(&h->dbg_anc, KT * 8), h->err);
@@ -821,6 +895,211 @@ int pf_get_debug(pf_handle* h, int32_t track, int64_t* anc, void* loglik) {
   if (loglik)
     PF_CUDA(cudaMemcpy(loglik, (char*)h->dbg_L + track * K * h->rs, K * h->rs, cudaMemcpyDeviceToHost), h->err);
   return PF_OK;
+}
+
+// ---------------------------------------------------------------------------
+// sharded filter: one track split by particle range over
+// n_shards handles; the host runs the three per-frame exchanges (NCCL
+// all-gathers on the handle's stream, or pf_shard_local_allgather for shards
+// that share a process)
+// ---------------------------------------------------------------------------
+int pf_shard_create(pf_handle** out, const pf_config* cfg, int32_t n_shards, int32_t shard) {
+  return create_impl(out, cfg, n_shards, shard);
+}
+
+int pf_shard_info(const pf_handle* h, int64_t* out4) {
+  if (!h || !out4) return PF_EINVAL;
+  out4[0] = h->shard_tiles;
+  out4[1] = h->tile0;
+  out4[2] = h->nl;
+  out4[3] = h->Kl;
+  return PF_OK;
+}
+
+int pf_shard_buffers(pf_handle* h, void** out8) {
+  if (!h || !out8) return PF_EINVAL;
+  for (int i = 0; i < 8; ++i) out8[i] = h->peer[h->shard][i];
+  return PF_OK;
+}
+
+int pf_shard_ipc_export(pf_handle* h, void* out) {
+  if (!h || !out) return PF_EINVAL;
+  PF_CUDA(cudaSetDevice(h->device), h->err);
+  cudaIpcMemHandle_t* o = reinterpret_cast<cudaIpcMemHandle_t*>(out);
+  for (int i = 0; i < 8; ++i) PF_CUDA(cudaIpcGetMemHandle(&o[i], h->peer[h->shard][i]), h->err);
+  return PF_OK;
+}
+
+int pf_shard_set_peer(pf_handle* h, int32_t peer, void* const* ptrs8) {
+  if (!h || !ptrs8 || peer < 0 || peer >= h->n_shards || peer == h->shard) return PF_EINVAL;
+  for (int i = 0; i < 8; ++i) h->peer[peer][i] = ptrs8[i];
+  return PF_OK;
+}
+
+int pf_shard_open_peer(pf_handle* h, int32_t peer, const void* handles) {
+  if (!h || !handles || peer < 0 || peer >= h->n_shards || peer == h->shard) return PF_EINVAL;
+  PF_CUDA(cudaSetDevice(h->device), h->err);
+  const cudaIpcMemHandle_t* in = reinterpret_cast<const cudaIpcMemHandle_t*>(handles);
+  for (int i = 0; i < 8; ++i)
+    PF_CUDA(cudaIpcOpenMemHandle(&h->peer[peer][i], in[i], cudaIpcMemLazyEnablePeerAccess), h->err);
+  h->peer_ipc[peer] = true;
+  return PF_OK;
+}
+
+int pf_shard_exchange(pf_handle* h, void** out4) {
+  if (!h || !out4 || h->n_shards < 2) return PF_EINVAL;
+  out4[0] = h->tsync;    // uint64 max key (send, 8 B)
+  out4[1] = h->sh_gmax;  // uint64 [n_shards] (receive)
+  out4[2] = h->sh_send;  // int64 [4] (send)
+  out4[3] = h->sh_gsum;  // int64 [n_shards][4] (receive)
+  return PF_OK;
+}
+
+void* pf_shard_stream(pf_handle* h) { return h ? (void*)h->stream : nullptr; }
+
+int pf_shard_begin(pf_handle* h, const uint8_t* frames, int32_t F, int32_t on_device) {
+  if (!h || !frames || F < 1 || h->n_shards < 2) return PF_EINVAL;
+  PF_CUDA(cudaSetDevice(h->device), h->err);
+  h->launches = 0;
+  const size_t fbytes = (size_t)F * h->H * h->W;
+  const size_t map_elems = (size_t)h->Hm * h->Wm;
+  int rc;
+  if ((rc = grow((void**)&h->d_maps, &h->maps_cap, (size_t)F * map_elems * h->rs, h->err))) return rc;
+  if ((rc = grow((void**)&h->d_traj, &h->traj_cap, (size_t)F * 2 * 8, h->err))) return rc;
+  const uint8_t* dframes = frames;
+  if (!on_device) {
+    if ((rc = grow((void**)&h->d_frames, &h->frames_cap, fbytes, h->err))) return rc;
+    PF_CUDA(cudaMemcpyAsync(h->d_frames, frames, fbytes, cudaMemcpyHostToDevice, h->stream), h->err);
+    dframes = h->d_frames;
+  }
+  PF_CUDA(cudaEventRecord(h->ev[0], h->stream), h->err);
+  if ((rc = launch_maps(h, dframes, F))) return rc;
+  h->sh_F = F;
+  return PF_OK;
+}
+
+int pf_shard_fused(pf_handle* h, int32_t f) {
+  if (!h || h->n_shards < 2 || f < 0 || f >= h->sh_F) return PF_EINVAL;
+  PF_CUDA(cudaSetDevice(h->device), h->err);
+  const size_t map_elems = (size_t)h->Hm * h->Wm;
+  const char* slot = (const char*)h->d_maps + (size_t)f * map_elems * h->rs;
+  return launch_frame(h, slot, (long long)h->sh_F * map_elems, f, h->sh_F);
+}
+
+static pfk::ShardArgs shard_args(pf_handle* h, int f) {
+  pfk::ShardArgs a{};
+  a.K = h->K;
+  a.n_tiles = h->n_tiles;
+  a.n_local = h->nl;
+  a.tile0 = h->tile0;
+  a.Q = h->Q;
+  a.n_shards = h->n_shards;
+  a.shard = h->shard;
+  a.n_chunks = h->sh_chunks;
+  a.gmax = h->sh_gmax;
+  a.gsum = h->sh_gsum;
+  a.rec_m = h->rec_m;
+  a.rec_S = h->rec_S;
+  a.rec_X = h->rec_X;
+  a.rec_Y = h->rec_Y;
+  a.mass = h->sh_mass;
+  a.ctot = h->sh_ctot;
+  a.croots = h->sh_croots;
+  a.sendsum = h->sh_send;
+  a.maxkey = h->tsync;
+  a.tab_s = h->tab_s;
+  a.tab_O = h->tab_O;
+  a.tab_invM = h->tab_invM;
+  a.win.n_shards = h->n_shards;
+  a.win.shard_tiles = h->shard_tiles;
+  for (int sh = 0; sh < h->n_shards; ++sh) a.win.win[sh] = (int2*)h->peer[sh][7];
+  a.u_out = h->u;
+  const pfr::Affine fu =
+      pfr::affine_pow((unsigned long long)h->frame_counter * (2ULL * h->K + 1) + 2ULL * (unsigned long long)h->K);
+  a.ua = fu.a;
+  a.uc = fu.c;
+  a.x0 = h->x0;
+  a.traj = h->d_traj;
+  a.traj_index = f;
+  a.degenerate = h->d_degen;
+  a.t = (int)h->frame_counter;
+  return a;
+}
+
+int pf_shard_tables(pf_handle* h) {
+  if (!h || h->n_shards < 2) return PF_EINVAL;
+  PF_CUDA(cudaSetDevice(h->device), h->err);
+  const pfk::ShardArgs a = shard_args(h, 0);
+  const int km = h->km;
+  if (km == 0) {
+    pfk::pf_shard_mass<0><<<h->sh_chunks, pfk::kShardChunk, 0, h->stream>>>(a);
+    pfk::pf_shard_sum<0><<<1, 1024, 0, h->stream>>>(a);
+  } else if (km == 1) {
+    pfk::pf_shard_mass<1><<<h->sh_chunks, pfk::kShardChunk, 0, h->stream>>>(a);
+    pfk::pf_shard_sum<1><<<1, 1024, 0, h->stream>>>(a);
+  } else {
+    pfk::pf_shard_mass<2><<<h->sh_chunks, pfk::kShardChunk, 0, h->stream>>>(a);
+    pfk::pf_shard_sum<2><<<1, 1024, 0, h->stream>>>(a);
+  }
+  PF_CUDA(cudaGetLastError(), h->err);
+  h->launches += 2;
+  return PF_OK;
+}
+
+int pf_shard_finish(pf_handle* h, int32_t f) {
+  if (!h || h->n_shards < 2 || f < 0 || f >= h->sh_F) return PF_EINVAL;
+  PF_CUDA(cudaSetDevice(h->device), h->err);
+  const pfk::ShardArgs a = shard_args(h, f);
+  if (h->km == 0)
+    pfk::pf_shard_finish<0><<<h->sh_chunks, pfk::kShardChunk, 0, h->stream>>>(a);
+  else if (h->km == 1)
+    pfk::pf_shard_finish<1><<<h->sh_chunks, pfk::kShardChunk, 0, h->stream>>>(a);
+  else
+    pfk::pf_shard_finish<2><<<h->sh_chunks, pfk::kShardChunk, 0, h->stream>>>(a);
+  PF_CUDA(cudaGetLastError(), h->err);
+  h->launches += 1;
+  h->cur = 1 - h->cur;
+  h->frame_counter += 1;
+  return PF_OK;
+}
+
+int pf_shard_end(pf_handle* h, int32_t F, double* traj_out) {
+  if (!h || h->n_shards < 2 || F < 1 || F > h->sh_F || !traj_out) return PF_EINVAL;
+  PF_CUDA(cudaSetDevice(h->device), h->err);
+  PF_CUDA(cudaEventRecord(h->ev[3], h->stream), h->err);
+  PF_CUDA(cudaMemcpyAsync(traj_out, h->d_traj, (size_t)F * 2 * 8, cudaMemcpyDeviceToHost, h->stream), h->err);
+  PF_CUDA(cudaEventRecord(h->ev[4], h->stream), h->err);
+  PF_CUDA(cudaStreamSynchronize(h->stream), h->err);
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, h->ev[0], h->ev[4]);
+  h->timings[0] = ms;
+  return finish_degenerate(h);
+}
+
+int pf_shard_local_allgather(pf_handle* const* hs, int32_t S, int32_t which) {
+  if (!hs || S < 2 || S > PF_MAX_SHARDS || which < 0 || which > 2) return PF_EINVAL;
+  for (int r = 0; r < S; ++r)
+    if (!hs[r] || hs[r]->n_shards != S || hs[r]->shard != r) return PF_EINVAL;
+  auto cross_wait = [&]() -> int {
+    for (int r = 0; r < S; ++r) {
+      PF_CUDA(cudaSetDevice(hs[r]->device), hs[r]->err);
+      PF_CUDA(cudaEventRecord(hs[r]->xev, hs[r]->stream), hs[r]->err);
+    }
+    for (int r = 0; r < S; ++r)
+      for (int q = 0; q < S; ++q)
+        if (q != r) PF_CUDA(cudaStreamWaitEvent(hs[r]->stream, hs[q]->xev, 0), hs[r]->err);
+    return PF_OK;
+  };
+  int rc = cross_wait();
+  if (rc || which == 2) return rc;
+  for (int r = 0; r < S; ++r) {
+    for (int q = 0; q < S; ++q) {
+      void* dst = which == 0 ? (void*)(hs[r]->sh_gmax + q) : (void*)(hs[r]->sh_gsum + 4 * q);
+      const void* src = which == 0 ? (const void*)hs[q]->tsync : (const void*)hs[q]->sh_send;
+      PF_CUDA(cudaMemcpyAsync(dst, src, which == 0 ? 8 : 32, cudaMemcpyDeviceToDevice, hs[r]->stream), hs[r]->err);
+    }
+  }
+  return cross_wait();  // no source is overwritten before every shard copied it
 }
 
 // ---------------------------------------------------------------------------

@@ -23,6 +23,7 @@
 #include "pf_rng.cuh"
 
 #define PF_TILE 1024
+#define PF_MAX_SHARDS 8
 #define PF_XQ_BITS 10
 
 namespace pfk {
@@ -275,18 +276,31 @@ __device__ __forceinline__ double point_of(long long k, double u, long long K, d
 // ------------------------------------------------------------------------
 // fused frame kernel
 // ------------------------------------------------------------------------
+// Source tiles of a frame's resampling may live on other shards of a
+// sharded filter: every source-tile access goes through the
+// per-shard base pointers below (peer-mapped over NVLink, or the handle's own
+// buffers when unsharded, n_shards == 1).
+struct SrcShards {
+  int n_shards;     // 1 = unsharded
+  int shard_tiles;  // tiles per shard (all but the last shard are full)
+  const void* X[PF_MAX_SHARDS];  // previous-frame positions
+  const void* C[PF_MAX_SHARDS];  // previous-frame local CDFs
+  const long long* ts[PF_MAX_SHARDS];
+  const double* tO[PF_MAX_SHARDS];
+  const double* tM[PF_MAX_SHARDS];
+};
+
 struct FusedArgs {
-  long long K;
-  int n_tiles;
+  long long K;        // particles per track (global, over all shards)
+  int n_tiles;        // tiles per track (global)
+  long long K_local;  // particles per track held by this handle
+  int n_local;        // tiles per track held by this handle
+  int tile0;          // global index of this handle's first tile
+  SrcShards src;
   int H, W, r, Wm;
   int t;  // frame index in the stream (RNG position, t==0 -> identity ancestors)
-  const void* X_prev;
   void* X_new;
-  const void* C_prev;
   void* C_new;
-  const long long* tab_s;
-  const double* tab_O;
-  const double* tab_invM;
   const double* u_prev;
   const void* map;             // map of video 0 for this frame
   long long map_video_stride;  // elements
@@ -733,20 +747,52 @@ __global__ void __launch_bounds__(PF_TILE / (VPT * R)) pf_fused_frame(FusedArgs 
   int* s_int = reinterpret_cast<int*>(s_misc + 192);  // b_lo, b_hi, staged, queue count
 
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-  const int tile = blockIdx.x, track = blockIdx.y;
-  const int K = (int)a.K;
-  const int base = tile * PF_TILE;
+  const int ltile = blockIdx.x, track = blockIdx.y;  // local tile of this handle
+  const int tile = a.tile0 + ltile;                   // global tile
+  const int K = (int)a.K, Kl = (int)a.K_local;
+  const int base = tile * PF_TILE;  // global index of the tile's first particle
+  const int lbase = ltile * PF_TILE;
   const int Tb = min(PF_TILE, K - base);
-  const int n = a.n_tiles;
+  const int n = a.n_tiles, nl = a.n_local;
 
-  const vec* __restrict__ Xp = reinterpret_cast<const vec*>(a.X_prev) + (size_t)track * K;
-  vec* __restrict__ Xn = reinterpret_cast<vec*>(a.X_new) + (size_t)track * K;
-  const real* __restrict__ Cp = reinterpret_cast<const real*>(a.C_prev) + (size_t)track * K;
-  real* __restrict__ Cn = reinterpret_cast<real*>(a.C_new) + (size_t)track * K;
+  vec* __restrict__ Xn = reinterpret_cast<vec*>(a.X_new) + (size_t)track * Kl;
+  real* __restrict__ Cn = reinterpret_cast<real*>(a.C_new) + (size_t)track * Kl;
   const real* __restrict__ map = reinterpret_cast<const real*>(a.map) + (size_t)(track % a.n_videos) * a.map_video_stride;
-  const long long* ts = a.tab_s + (size_t)track * n;
-  const double* tO = a.tab_O + (size_t)track * n;
-  const double* tM = a.tab_invM + (size_t)track * n;
+  // source tile b (global) -> (shard, local tile); track offsets apply when unsharded
+  auto shard_of = [&](int b, int& lb) -> int {
+    if (a.src.n_shards == 1) {
+      lb = b;
+      return 0;
+    }
+    const int sh = b / a.src.shard_tiles;
+    lb = b - sh * a.src.shard_tiles;
+    return sh;
+  };
+  auto src_X = [&](int b) -> const vec* {
+    int lb;
+    const int sh = shard_of(b, lb);
+    return reinterpret_cast<const vec*>(a.src.X[sh]) + (size_t)track * Kl + (size_t)lb * PF_TILE;
+  };
+  auto src_C = [&](int b) -> const real* {
+    int lb;
+    const int sh = shard_of(b, lb);
+    return reinterpret_cast<const real*>(a.src.C[sh]) + (size_t)track * Kl + (size_t)lb * PF_TILE;
+  };
+  auto g_ts = [&](int b) -> int {
+    int lb;
+    const int sh = shard_of(b, lb);
+    return (int)__ldg(a.src.ts[sh] + (size_t)track * nl + lb);
+  };
+  auto g_tO = [&](int b) -> double {
+    int lb;
+    const int sh = shard_of(b, lb);
+    return __ldg(a.src.tO[sh] + (size_t)track * nl + lb);
+  };
+  auto g_tM = [&](int b) -> double {
+    int lb;
+    const int sh = shard_of(b, lb);
+    return __ldg(a.src.tM[sh] + (size_t)track * nl + lb);
+  };
 
   {
     const uint4* zsrc = reinterpret_cast<const uint4*>(a.zig);
@@ -758,7 +804,7 @@ __global__ void __launch_bounds__(PF_TILE / (VPT * R)) pf_fused_frame(FusedArgs 
   // stream state at this tile's first draw, position t(2K+1) + 2*base: the
   // frame's affine jump (kernel argument) and the per-tile jump
   const unsigned long long tstate =
-      pfr::apply(pfr::Affine{a.tt[tile].x, a.tt[tile].y}, a.fa * a.x0[track] + a.fc);
+      pfr::apply(pfr::Affine{a.tt[ltile].x, a.tt[ltile].y}, a.fa * a.x0[track] + a.fc);
   pdl_launch_dependents();
   __syncthreads();
 
@@ -827,7 +873,7 @@ __global__ void __launch_bounds__(PF_TILE / (VPT * R)) pf_fused_frame(FusedArgs 
   //      CDFs while it fetches their table entries; the other warps meanwhile
   //      resolve the queued slow paths ------------------------------------
   uint64_t* s_bar = reinterpret_cast<uint64_t*>(s_misc + 200);
-  const bool bulk_ok = ((((size_t)track * K) * sizeof(real)) % 16) == 0;
+  const bool bulk_ok = ((((size_t)track * Kl) * sizeof(real)) % 16) == 0;
   if (wid == 0 || NW == 1) {
     if (a.t > 0) {  // acquire the previous frame's table (published before its grid ends)
       if (lane == 0) {
@@ -849,22 +895,31 @@ __global__ void __launch_bounds__(PF_TILE / (VPT * R)) pf_fused_frame(FusedArgs 
     }
     PF_TRACE(a, 2);
     if (a.t > 0) {
-      const int2 wn = __ldcg(reinterpret_cast<const int2*>(a.win) + (size_t)track * n + tile);
+      const int2 wn = __ldcg(reinterpret_cast<const int2*>(a.win) + (size_t)track * nl + ltile);
       const int nsrc = wn.y - wn.x + 1;
       const int staged = nsrc <= MS ? 1 : 0;
-      if (staged && bulk_ok && lane == 0) {
-        const int c0 = wn.x * PF_TILE;
-        const int cnt = min((wn.y + 1) * PF_TILE, K) - c0;
-        const uint32_t bytes = (uint32_t)((cnt * (int)sizeof(real) + 15) & ~15);  // C buffers carry 16 B of slack
+      if (staged && bulk_ok) {
+        // one bulk copy per source tile (tiles may live on different shards)
         const uint32_t bb = smem_u32(s_bar);
-        asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bb), "r"(1) : "memory");
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bb), "r"(bytes) : "memory");
-        asm volatile(
-            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                smem_u32(s_c)),
-            "l"(Cp + c0), "r"(bytes), "r"(bb)
-            : "memory");
+        if (lane == 0) {
+          uint32_t total = 0;
+          for (int e = 0; e < nsrc; ++e)
+            total += (uint32_t)((min(PF_TILE, K - (wn.x + e) * PF_TILE) * (int)sizeof(real) + 15) & ~15);
+          asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bb), "r"(1) : "memory");
+          asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+          asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bb), "r"(total) : "memory");
+        }
+        __syncwarp();
+        if (lane < nsrc) {
+          const int b = wn.x + lane;
+          // C buffers carry 16 B of slack for the rounded size
+          const uint32_t bytes = (uint32_t)((min(PF_TILE, K - b * PF_TILE) * (int)sizeof(real) + 15) & ~15);
+          asm volatile(
+              "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                  smem_u32(s_c + lane * PF_TILE)),
+              "l"(src_C(b)), "r"(bytes), "r"(bb)
+              : "memory");
+        }
       }
       if (lane == 0) {
         s_int[0] = wn.x;
@@ -873,9 +928,9 @@ __global__ void __launch_bounds__(PF_TILE / (VPT * R)) pf_fused_frame(FusedArgs 
       }
       if (staged && lane <= nsrc) {
         const int b = min(wn.x + lane, n - 1);
-        s_ts[lane] = lane < nsrc ? (int)__ldg(ts + b) : K;
-        s_tO[lane] = __ldg(tO + b);
-        s_tM[lane] = __ldg(tM + b);
+        s_ts[lane] = lane < nsrc ? g_ts(b) : K;
+        s_tO[lane] = g_tO(b);
+        s_tM[lane] = g_tM(b);
       }
     }
   }
@@ -904,20 +959,22 @@ __global__ void __launch_bounds__(PF_TILE / (VPT * R)) pf_fused_frame(FusedArgs 
             "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(s_bar))
             : "memory");
       } else {  // unaligned track base (odd K with several tracks): plain copy
-        const int c0 = b_lo * PF_TILE;
-        const int cnt = min((b_hi + 1) * PF_TILE, K) - c0;
-        for (int i = tid; i < cnt; i += TPB) s_c[i] = Cp[c0 + i];
+        for (int b = b_lo; b <= b_hi; ++b) {
+          const real* src = src_C(b);
+          const int cnt = min(PF_TILE, K - b * PF_TILE);
+          for (int i = tid; i < cnt; i += TPB) s_c[(b - b_lo) * PF_TILE + i] = src[i];
+        }
         __syncthreads();
       }
     }
   }
-  const real* Csrc = staged ? s_c - b_lo * PF_TILE : Cp;
-  const vec* Xsrc = Xp;
   const double invK = __ddiv_rn(1.0, (double)K);
 
-  auto tab_s = [&](int b) -> int { return staged ? s_ts[b - b_lo] : (int)__ldg(ts + b); };
-  auto tab_O = [&](int b) -> double { return staged ? s_tO[b - b_lo] : __ldg(tO + b); };
-  auto tab_M = [&](int b) -> double { return staged ? s_tM[b - b_lo] : __ldg(tM + b); };
+  auto tab_s = [&](int b) -> int { return staged ? s_ts[b - b_lo] : g_ts(b); };
+  auto tab_O = [&](int b) -> double { return staged ? s_tO[b - b_lo] : g_tO(b); };
+  auto tab_M = [&](int b) -> double { return staged ? s_tM[b - b_lo] : g_tM(b); };
+  // a source tile's local CDF: staged copy in shared memory, else its shard's buffer
+  auto tile_C = [&](int b) -> const real* { return staged ? s_c + (b - b_lo) * PF_TILE : src_C(b); };
 
   // ---- phase 1: resample + propagate + likelihood -------------------------
   real Lr[R][VPT];
@@ -926,17 +983,22 @@ __global__ void __launch_bounds__(PF_TILE / (VPT * R)) pf_fused_frame(FusedArgs 
 #pragma unroll
   for (int rr = 0; rr < R; ++rr) {
     const int l0 = (rr * TPB + tid) * VPT;
-    int anc[VPT];
-    if (a.t == 0 || l0 >= Tb) {
+    int anc[VPT];          // global ancestor index
+    const vec* asrc[VPT];  // its position (in its shard's buffer)
+    if (a.t == 0 || l0 >= Tb) {  // frame 0: identity ancestors (own shard)
 #pragma unroll
-      for (int i = 0; i < VPT; ++i) anc[i] = base + l0 + i;
+      for (int i = 0; i < VPT; ++i) {
+        anc[i] = base + l0 + i;
+        asrc[i] = reinterpret_cast<const vec*>(a.src.X[a.src.n_shards == 1 ? 0 : tile / a.src.shard_tiles]) +
+                  (size_t)track * Kl + lbase + l0 + i;
+      }
     } else {
       int b = b_lo;
       if (!staged) {
         int lo = b_lo, hi = b_hi;
         while (lo < hi) {
           const int mid = (lo + hi + 1) >> 1;
-          if ((int)__ldg(ts + mid) <= base + l0)
+          if (g_ts(mid) <= base + l0)
             lo = mid;
           else
             hi = mid - 1;
@@ -948,13 +1010,15 @@ __global__ void __launch_bounds__(PF_TILE / (VPT * R)) pf_fused_frame(FusedArgs 
       double gO = tab_O(b), gM = tab_M(b);
       float fO = (float)gO, fM = (float)gM;  // FP16: the table holds f32 values
       int tl = b * PF_TILE, tb = min(PF_TILE, K - tl);
-      const real* cb = Csrc + tl;
+      const real* cb = tile_C(b);
+      const vec* xb = src_X(b);
       int jprev = -1;
 #pragma unroll
       for (int i = 0; i < VPT; ++i) {
         const int k = base + l0 + i;
         if (k >= K) {
           anc[i] = k;
+          asrc[i] = xb;
           continue;
         }
         if (k >= snext) {  // next source tile (rare: outputs of one source tile are contiguous)
@@ -969,7 +1033,8 @@ __global__ void __launch_bounds__(PF_TILE / (VPT * R)) pf_fused_frame(FusedArgs 
           fM = (float)gM;
           tl = b * PF_TILE;
           tb = min(PF_TILE, K - tl);
-          cb = Csrc + tl;
+          cb = tile_C(b);
+          xb = src_X(b);
           jprev = -1;
         }
         typename KT::k_t kq;
@@ -986,12 +1051,13 @@ __global__ void __launch_bounds__(PF_TILE / (VPT * R)) pf_fused_frame(FusedArgs 
         j = min(j, tb - 1);
         jprev = j;
         anc[i] = tl + j;
+        asrc[i] = xb + j;
       }
     }
     if (a.dbg_anc != nullptr) {
 #pragma unroll
       for (int i = 0; i < VPT; ++i)
-        if (l0 + i < Tb) a.dbg_anc[(size_t)track * K + base + l0 + i] = anc[i];
+        if (l0 + i < Tb) a.dbg_anc[(size_t)track * Kl + lbase + l0 + i] = anc[i];
     }
     // all VPT ancestor gathers first (independent, read-only X_prev), then
     // propagation and all VPT map lookups, then the new positions' stores --
@@ -1000,7 +1066,7 @@ __global__ void __launch_bounds__(PF_TILE / (VPT * R)) pf_fused_frame(FusedArgs 
 #pragma unroll
     for (int i = 0; i < VPT; ++i) {
       if (l0 + i < Tb) {
-        xa[i] = __ldg(Xsrc + anc[i]);
+        xa[i] = __ldg(asrc[i]);
       } else {
         xa[i].x = (real)0;
         xa[i].y = (real)0;
@@ -1023,8 +1089,8 @@ __global__ void __launch_bounds__(PF_TILE / (VPT * R)) pf_fused_frame(FusedArgs 
     }
     {
       constexpr int VB = VPT * (int)sizeof(vec);
-      if (VB % 16 == 0 && l0 + VPT <= Tb && ((((size_t)track * K) * sizeof(vec)) % 16) == 0) {
-        uint4* dst = reinterpret_cast<uint4*>(Xn + base + l0);
+      if (VB % 16 == 0 && l0 + VPT <= Tb && ((((size_t)track * Kl) * sizeof(vec)) % 16) == 0) {
+        uint4* dst = reinterpret_cast<uint4*>(Xn + lbase + l0);
 #pragma unroll
         for (int q = 0; q < VB / 16; ++q) {
           uint4 o;
@@ -1034,7 +1100,7 @@ __global__ void __launch_bounds__(PF_TILE / (VPT * R)) pf_fused_frame(FusedArgs 
       } else {
 #pragma unroll
         for (int i = 0; i < VPT; ++i)
-          if (l0 + i < Tb) Xn[base + l0 + i] = Xr[rr][i];
+          if (l0 + i < Tb) Xn[lbase + l0 + i] = Xr[rr][i];
       }
     }
 #pragma unroll
@@ -1047,7 +1113,7 @@ __global__ void __launch_bounds__(PF_TILE / (VPT * R)) pf_fused_frame(FusedArgs 
       const int l0 = (rr * TPB + tid) * VPT;
 #pragma unroll
       for (int i = 0; i < VPT; ++i)
-        if (l0 + i < Tb) reinterpret_cast<real*>(a.dbg_L)[(size_t)track * K + base + l0 + i] = Lr[rr][i];
+        if (l0 + i < Tb) reinterpret_cast<real*>(a.dbg_L)[(size_t)track * Kl + lbase + l0 + i] = Lr[rr][i];
     }
   }
   PF_TRACE(a, 4);
@@ -1171,29 +1237,29 @@ __global__ void __launch_bounds__(PF_TILE / (VPT * R)) pf_fused_frame(FusedArgs 
 #pragma unroll
     for (int i = 0; i < VPT; ++i) cv[i] = cdf_of(pre[rr] + wexcl[rr] + cum[rr][i]);
     constexpr int VB = VPT * (int)sizeof(real);
-    if (l0 + VPT <= Tb && (VB == 4 || VB == 8 || VB == 16) && ((((size_t)track * K) * sizeof(real)) % VB) == 0) {
+    if (l0 + VPT <= Tb && (VB == 4 || VB == 8 || VB == 16) && ((((size_t)track * Kl) * sizeof(real)) % VB) == 0) {
       if constexpr (VB == 16) {
         uint4 o;
         memcpy(&o, cv, 16);
-        *reinterpret_cast<uint4*>(Cn + base + l0) = o;
+        *reinterpret_cast<uint4*>(Cn + lbase + l0) = o;
       } else if constexpr (VB == 8) {
         uint2 o;
         memcpy(&o, cv, 8);
-        *reinterpret_cast<uint2*>(Cn + base + l0) = o;
+        *reinterpret_cast<uint2*>(Cn + lbase + l0) = o;
       } else if constexpr (VB == 4) {
         unsigned o;
         memcpy(&o, cv, 4);
-        *reinterpret_cast<unsigned*>(Cn + base + l0) = o;
+        *reinterpret_cast<unsigned*>(Cn + lbase + l0) = o;
       }
     } else {
 #pragma unroll
       for (int i = 0; i < VPT; ++i)
-        if (l0 + i < Tb) Cn[base + l0 + i] = cv[i];
+        if (l0 + i < Tb) Cn[lbase + l0 + i] = cv[i];
     }
   }
   // tile record
   if (tid == 0) {
-    const size_t ri = (size_t)track * n + tile;
+    const size_t ri = (size_t)track * nl + ltile;
     a.rec_m[ri] = to_d(mtile);
     atomicMax(a.tmax + (size_t)track * 4, okey(to_d(mtile)));  // the table reads the track max directly
     a.rec_S[ri] = (long long)S;
@@ -1283,6 +1349,29 @@ __device__ __forceinline__ void spin_until(unsigned long long* ctr, unsigned lon
   while (atomicAdd(ctr, 0ULL) < target) __nanosleep(64);
 }
 
+// Source windows of the next frame (scatter): destination tile d starts
+// (ends) in source tile b iff its first (last) output index lies in
+// [s_b, s_{b+1}); the ranges partition [0, K), so every d is written exactly
+// once.  d is global; its record lives with the shard that owns it.
+struct WinShards {
+  int n_shards, shard_tiles;
+  int2* win[PF_MAX_SHARDS];
+};
+__device__ __forceinline__ void scatter_windows(const WinShards& w, size_t track_off, int n, long long K, int b,
+                                                long long sb, long long sn) {
+  auto first_lo = [&](long long x) -> long long { return min((long long)n, (x + PF_TILE - 1) / PF_TILE); };
+  auto first_hi = [&](long long x) -> long long {
+    return x >= K ? (long long)n : min((long long)n - 1, max(0LL, x / PF_TILE));  // last output of d is 1024d+1023
+  };
+  auto rec = [&](long long d) -> int2* {
+    if (w.n_shards == 1) return w.win[0] + track_off + d;
+    const int sh = (int)(d / w.shard_tiles);
+    return w.win[sh] + (d - (long long)sh * w.shard_tiles);
+  };
+  for (long long d = first_lo(sb), e = first_lo(sn); d < e; ++d) rec(d)->x = b;
+  for (long long d = first_hi(sb), e = first_hi(sn); d < e; ++d) rec(d)->y = b;
+}
+
 // Tile table, one CTA per chunk of blockDim.x tiles (one tile per thread),
 // grid (n_chunks, n_tracks).  All cross-CTA combination is exact: the global
 // max is an atomicMax over order-preserving keys, the mass prefix an int64
@@ -1369,6 +1458,7 @@ __global__ void __launch_bounds__(1024) pf_tile_table(TableArgs a) {
     __syncthreads();
   }
   const double Sq = (double)Sqi;
+  PF_TRACE(a, 6);
 
   // 3. table entries and the estimate moments
   double vx = 0.0, vy = 0.0, vd = 0.0;
@@ -1404,9 +1494,8 @@ __global__ void __launch_bounds__(1024) pf_tile_table(TableArgs a) {
     vy = __dmul_rn(f, Y);
     vd = __dmul_rn(f, (double)S1);
   }
-  // source windows of the next frame: destination tile d starts (ends) in
-  // source tile b iff its first (last) output index lies in [s_b, s_{b+1});
-  // the ranges partition [0, K), so every d is written exactly once
+  PF_TRACE(a, 7);
+  // source windows of the next frame (scatter_windows)
   __syncthreads();
   if (valid) {
     const long long sb = s_sb[tid];
@@ -1423,14 +1512,11 @@ __global__ void __launch_bounds__(1024) pf_tile_table(TableArgs a) {
       while (k < a.K && point_of<MODE>(k, u, a.K, invK) <= On) ++k;
       sn = k;
     }
-    const long long K = a.K;
-    auto first_lo = [&](long long x) -> long long { return min((long long)n, (x + PF_TILE - 1) / PF_TILE); };
-    auto first_hi = [&](long long x) -> long long {
-      return x >= K ? (long long)n : min((long long)n - 1, max(0LL, (x - (PF_TILE - 1) + PF_TILE - 1) / PF_TILE));
-    };
-    int2* wt = a.win + (size_t)track * n;
-    for (long long d = first_lo(sb), e = first_lo(sn); d < e; ++d) wt[d].x = b;
-    for (long long d = first_hi(sb), e = first_hi(sn); d < e; ++d) wt[d].y = b;
+    WinShards ws;
+    ws.n_shards = 1;
+    ws.shard_tiles = n;
+    ws.win[0] = a.win;
+    scatter_windows(ws, (size_t)track * n, n, a.K, b, sb, sn);
   }
   // early release of the next frame: table entries, windows and u are
   // published with a per-track monotone counter (sy[1], +1 per chunk); the
@@ -1440,9 +1526,11 @@ __global__ void __launch_bounds__(1024) pf_tile_table(TableArgs a) {
     a.u_out[track] = u;
     if (nc == 1) sy[0] = 0;  // all threads read the max key before the barrier above
   }
-  __threadfence();
-  __syncthreads();
-  if (tid == 0) atomicAdd(sy + 1, 1ULL);
+  __syncthreads();  // CTA-wide release: barrier, then one gpu-scope fence + the counter
+  if (tid == 0) {
+    __threadfence();
+    atomicAdd(sy + 1, 1ULL);
+  }
   PF_TRACE(a, 5);
   // canonical pairwise tree: lanes, warps (zero padded), chunks (last CTA)
 #pragma unroll
@@ -1550,6 +1638,285 @@ __global__ void __launch_bounds__(1024) pf_tile_table(TableArgs a) {
       sy[3] = 0;
     }
     __threadfence();
+  }
+}
+
+// ------------------------------------------------------------------------
+// Sharded filter tables: one track split by particle range
+// over n_shards handles (GPUs).  Per frame, on every shard, stream-ordered:
+//   fused kernel -> [all-gather of the max keys]
+//   -> pf_shard_mass (chunks of 256 tiles: exact masses, chunk totals, chunk
+//      moment subtrees) -> pf_shard_sum (one CTA: chunk prefixes, shard total,
+//      shard subtree roots) -> [all-gather of (total, X, Y, D)]
+//   -> pf_shard_finish (offsets, table entries, window scatter into the owning
+//      shards' records, estimate from the shard roots) -> [barrier]
+// Every combination is the single-GPU table's (exact int64 prefixes, the
+// canonical pairwise tree over tiles: shard_tiles is a power of two, so each
+// shard's root is a node of the global tree), so the sharded filter is
+// bit-identical to the same filter on one GPU.
+// ------------------------------------------------------------------------
+constexpr int kShardChunk = 256;
+
+struct ShardArgs {
+  long long K;      // global particles
+  int n_tiles;      // global tiles
+  int n_local;      // this shard's tiles
+  int tile0;        // global index of this shard's first tile
+  int Q;
+  int n_shards, shard;
+  int n_chunks;     // local chunks of kShardChunk tiles
+  const unsigned long long* gmax;  // [n_shards] gathered max keys
+  const long long* gsum;           // [n_shards][4] gathered: mass total, X, Y, D roots (double bits)
+  const double* rec_m;
+  const long long* rec_S;
+  const long long* rec_X;
+  const long long* rec_Y;
+  long long* mass;       // [n_local] scratch: tile masses
+  long long* ctot;       // [n_chunks]: chunk mass totals, then (pf_shard_sum) chunk exclusive prefixes
+  double* croots;        // [n_chunks][3]: chunk moment subtree roots
+  long long* sendsum;    // [4]: this shard's contribution to the second all-gather
+  unsigned long long* maxkey;  // the fused kernels' max key (reset once gathered)
+  long long* tab_s;
+  double* tab_O;
+  double* tab_invM;
+  WinShards win;
+  double* u_out;
+  unsigned long long ua, uc;
+  const unsigned long long* x0;
+  double* traj;
+  int traj_index;
+  int* degenerate;
+  int t;
+};
+
+template <int MODE>
+__global__ void __launch_bounds__(kShardChunk) pf_shard_mass(ShardArgs a) {
+  constexpr int FB = Tr<MODE>::FB;
+  __shared__ long long s_i[kShardChunk / 32];
+  __shared__ double s_d[3 * 32];
+  const int chunk = blockIdx.x, tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, nw = kShardChunk / 32;
+  const int b = chunk * kShardChunk + tid;  // local tile
+  const bool valid = b < a.n_local;
+  unsigned long long mk = 0;
+  for (int sh = 0; sh < a.n_shards; ++sh) mk = max(mk, a.gmax[sh]);
+  const double m = okey_inv(mk);
+  double vx = 0.0, vy = 0.0, vd = 0.0;
+  long long mass = 0;
+  if (valid) {
+    const double m1 = a.rec_m[b];
+    const long long S1 = a.rec_S[b];
+    const double f = pfm::exp64(__dsub_rn(m1, m));
+    mass = __double2ll_rn(__dmul_rn(__dmul_rn((double)S1, f), ldexp(1.0, a.Q - FB)));
+    double X, Y;
+    if constexpr (MODE == M_FP16) {
+      X = (double)a.rec_X[b];
+      Y = (double)a.rec_Y[b];
+    } else {
+      X = __longlong_as_double(a.rec_X[b]);
+      Y = __longlong_as_double(a.rec_Y[b]);
+    }
+    vx = __dmul_rn(f, X);
+    vy = __dmul_rn(f, Y);
+    vd = __dmul_rn(f, (double)S1);
+    a.mass[b] = mass;
+  }
+  // exact chunk total
+  long long tot = mass;
+#pragma unroll
+  for (int d = 16; d >= 1; d >>= 1) tot += __shfl_xor_sync(0xffffffffu, tot, d);
+  // canonical pairwise tree over the chunk's 256 tiles: lanes, then warps (zero padded)
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    vx = __dadd_rn(vx, __shfl_xor_sync(0xffffffffu, vx, d));
+    vy = __dadd_rn(vy, __shfl_xor_sync(0xffffffffu, vy, d));
+    vd = __dadd_rn(vd, __shfl_xor_sync(0xffffffffu, vd, d));
+  }
+  if (lane == 0) {
+    s_i[wid] = tot;
+    s_d[wid] = vx;
+    s_d[32 + wid] = vy;
+    s_d[64 + wid] = vd;
+  }
+  __syncthreads();
+  if (wid == 0) {
+    long long ct = lane < nw ? s_i[lane] : 0;
+    vx = lane < nw ? s_d[lane] : 0.0;
+    vy = lane < nw ? s_d[32 + lane] : 0.0;
+    vd = lane < nw ? s_d[64 + lane] : 0.0;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      ct += __shfl_xor_sync(0xffffffffu, ct, d);
+      vx = __dadd_rn(vx, __shfl_xor_sync(0xffffffffu, vx, d));
+      vy = __dadd_rn(vy, __shfl_xor_sync(0xffffffffu, vy, d));
+      vd = __dadd_rn(vd, __shfl_xor_sync(0xffffffffu, vd, d));
+    }
+    if (lane == 0) {
+      a.ctot[chunk] = ct;
+      a.croots[3 * chunk + 0] = vx;
+      a.croots[3 * chunk + 1] = vy;
+      a.croots[3 * chunk + 2] = vd;
+    }
+  }
+}
+
+// one CTA: chunk exclusive prefixes (exact), shard total, shard subtree roots
+template <int MODE>
+__global__ void __launch_bounds__(1024) pf_shard_sum(ShardArgs a) {
+  __shared__ long long s_i[32];
+  __shared__ double s_d[3 * 32];
+  __shared__ long long s_carry;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, TPB = blockDim.x, nw = TPB >> 5;
+  const int nc = a.n_chunks;
+  if (tid == 0) {
+    s_carry = 0;
+    *a.maxkey = 0;  // gathered: the next frame's fused CTAs publish into a fresh key
+  }
+  __syncthreads();
+  // exclusive prefix of chunk totals, TPB at a time
+  for (int c0 = 0; c0 < nc; c0 += TPB) {
+    const int c = c0 + tid;
+    const long long v = c < nc ? a.ctot[c] : 0;
+    long long tot;
+    const long long ex = block_excl_scan<long long>(v, s_i, &tot);
+    const long long carry = s_carry;
+    if (c < nc) a.ctot[c] = carry + ex;
+    __syncthreads();
+    if (tid == 0) s_carry = carry + tot;
+    __syncthreads();
+  }
+  // canonical tree over the chunk roots (power-of-two padded): each thread a
+  // contiguous pow2 block, then butterflies
+  int ncp = 1;
+  while (ncp < nc) ncp <<= 1;
+  const int per = max(1, ncp / TPB);
+  double px = 0.0, py = 0.0, pd = 0.0;
+  if (tid * per < ncp) {
+    PwAcc ax, ay, ad;
+    ax.reset();
+    ay.reset();
+    ad.reset();
+    for (int e = 0; e < per; ++e) {
+      const int c = tid * per + e;
+      ax.push(c < nc ? a.croots[3 * c] : 0.0);
+      ay.push(c < nc ? a.croots[3 * c + 1] : 0.0);
+      ad.push(c < nc ? a.croots[3 * c + 2] : 0.0);
+    }
+    px = ax.root();
+    py = ay.root();
+    pd = ad.root();
+  }
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    px = __dadd_rn(px, __shfl_xor_sync(0xffffffffu, px, d));
+    py = __dadd_rn(py, __shfl_xor_sync(0xffffffffu, py, d));
+    pd = __dadd_rn(pd, __shfl_xor_sync(0xffffffffu, pd, d));
+  }
+  if (lane == 0) {
+    s_d[wid] = px;
+    s_d[32 + wid] = py;
+    s_d[64 + wid] = pd;
+  }
+  __syncthreads();
+  if (wid == 0) {
+    px = lane < nw ? s_d[lane] : 0.0;
+    py = lane < nw ? s_d[32 + lane] : 0.0;
+    pd = lane < nw ? s_d[64 + lane] : 0.0;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      px = __dadd_rn(px, __shfl_xor_sync(0xffffffffu, px, d));
+      py = __dadd_rn(py, __shfl_xor_sync(0xffffffffu, py, d));
+      pd = __dadd_rn(pd, __shfl_xor_sync(0xffffffffu, pd, d));
+    }
+    if (lane == 0) {
+      a.sendsum[0] = s_carry;
+      a.sendsum[1] = __double_as_longlong(px);
+      a.sendsum[2] = __double_as_longlong(py);
+      a.sendsum[3] = __double_as_longlong(pd);
+    }
+  }
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(kShardChunk) pf_shard_finish(ShardArgs a) {
+  __shared__ long long s_i[32];
+  __shared__ long long s_sb[kShardChunk];
+  const int chunk = blockIdx.x, tid = threadIdx.x;
+  const int bl = chunk * kShardChunk + tid;  // local tile
+  const int b = a.tile0 + bl;                // global tile
+  const bool valid = bl < a.n_local;
+  const int n = a.n_tiles;
+  long long offset = 0, all = 0;
+  for (int sh = 0; sh < a.n_shards; ++sh) {
+    const long long v = a.gsum[4 * sh];
+    if (sh < a.shard) offset += v;
+    all += v;
+  }
+  const double Sq = (double)all;
+  const double Kd = __ll2double_rn(a.K);
+  const double invK = __ddiv_rn(1.0, Kd);
+  const double u = pfr::uniform_of(a.ua * a.x0[0] + a.uc);
+  const long long mass = valid ? a.mass[bl] : 0;
+  long long ctot;
+  long long excl = block_excl_scan<long long>(mass, s_i, &ctot) + offset + a.ctot[chunk];
+  auto s_of = [&](double O) -> long long {
+    long long k = (long long)floor(__dsub_rn(__dmul_rn(O, Kd), u));
+    k = min(max(k, 0LL), a.K);
+    while (k > 0 && point_of<MODE>(k - 1, u, a.K, invK) > O) --k;
+    while (k < a.K && point_of<MODE>(k, u, a.K, invK) <= O) ++k;
+    return k;
+  };
+  long long sb = 0;
+  if (valid) {
+    const double O = __ddiv_rn((double)excl, Sq);
+    if (b > 0) sb = s_of(O);
+    a.tab_s[bl] = sb;
+    if constexpr (MODE == M_FP16) {
+      a.tab_O[bl] = (double)__double2float_rn(__dsub_rn(__dadd_rn((double)sb, u), __dmul_rn(Kd, O)));
+      a.tab_invM[bl] = mass > 0 ? (double)__double2float_rn(__ddiv_rn(Sq, __dmul_rn(Kd, (double)mass))) : 0.0;
+    } else {
+      a.tab_O[bl] = O;
+      a.tab_invM[bl] = mass > 0 ? __ddiv_rn(Sq, (double)mass) : 0.0;
+    }
+    s_sb[tid] = sb;
+  }
+  __syncthreads();
+  if (valid) {
+    long long sn;
+    if (b + 1 >= n)
+      sn = a.K;
+    else if (tid + 1 < kShardChunk && bl + 1 < a.n_local)
+      sn = s_sb[tid + 1];
+    else  // first tile of the next chunk / shard: same formula on its exact prefix
+      sn = s_of(__ddiv_rn((double)(excl + mass), Sq));
+    scatter_windows(a.win, 0, n, a.K, b, sb, sn);
+  }
+  if (chunk == 0 && tid == 0) {
+    // estimate: canonical tree over the shard roots (power-of-two padded)
+    double vx[PF_MAX_SHARDS], vy[PF_MAX_SHARDS], vd[PF_MAX_SHARDS];
+    int w = 1;
+    while (w < a.n_shards) w <<= 1;
+    for (int sh = 0; sh < w; ++sh) {
+      const bool ok = sh < a.n_shards;
+      vx[sh] = ok ? __longlong_as_double(a.gsum[4 * sh + 1]) : 0.0;
+      vy[sh] = ok ? __longlong_as_double(a.gsum[4 * sh + 2]) : 0.0;
+      vd[sh] = ok ? __longlong_as_double(a.gsum[4 * sh + 3]) : 0.0;
+    }
+    for (; w > 1; w >>= 1)
+      for (int e = 0; e < w / 2; ++e) {
+        vx[e] = __dadd_rn(vx[2 * e], vx[2 * e + 1]);
+        vy[e] = __dadd_rn(vy[2 * e], vy[2 * e + 1]);
+        vd[e] = __dadd_rn(vd[2 * e], vd[2 * e + 1]);
+      }
+    double ex = __ddiv_rn(vx[0], vd[0]);
+    double ey = __ddiv_rn(vy[0], vd[0]);
+    if constexpr (MODE == M_FP16) {
+      ex = __dmul_rn(ex, 1.0 / 1024.0);
+      ey = __dmul_rn(ey, 1.0 / 1024.0);
+    }
+    a.traj[2 * a.traj_index] = ex;
+    a.traj[2 * a.traj_index + 1] = ey;
+    *a.u_out = u;
+    if (!(vd[0] > 0.0) || !isfinite(vd[0]) || !isfinite(ex) || !isfinite(ey)) atomicMin(a.degenerate, a.t);
   }
 }
 

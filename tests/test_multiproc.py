@@ -65,3 +65,73 @@ def test_gloo_two_ranks():
     for rank, tracks, m in res:
         assert tracks == [0.0, 1.0, 2.0, 3.0, 4.0]
         assert m == 11.0
+
+
+# ---- sharded giant filter (C5): the exchange protocol on gloo --------------
+class _GlooComm:
+    def __init__(self, dist_):
+        self.dist = dist_
+
+    def allgather(self, obj):
+        out = [None] * self.dist.get_world_size()
+        self.dist.all_gather_object(out, obj)
+        return out
+
+
+def _shard_worker(rank, world, port, q, K, mode):
+    import sys
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from oracle import reference_port as rp
+        from oracle import sharded
+
+        frames, _ = rp.generate_video(rp.Params(), 4, 64, 48, (30.0, 20.0), 11)
+        traj = sharded.run_shard(frames, K, mode, 9, rank, world, _GlooComm(dist))
+        q.put((rank, traj))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("mode,K", [("fp16", 5000), ("fp64", 3100), ("fp32", 4097)])
+def test_gloo_sharded_filter_protocol_equals_single(mode, K):
+    """Two ranks, one filter split by particle range, exchanging only the max,
+    (mass total, subtree roots) and peer-read table/CDF/positions: equals the
+    unsharded fused algorithm bit-for-bit."""
+    from oracle import fused
+    from oracle import reference_port as rp
+
+    frames, _ = rp.generate_video(rp.Params(), 4, 64, 48, (30.0, 20.0), 11)
+    ref, _ = fused.run(frames, K, mode, 9)
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_shard_worker, args=(r, 2, port, q, K, mode)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=300) for _ in procs]
+    for p in procs:
+        p.join(timeout=60)
+    for rank, traj in res:
+        assert np.array_equal(traj, ref), (rank, traj[:2], ref[:2])
+
+
+def test_shard_layout_matches_library_rule():
+    from oracle.sharded import shard_tiles
+    from paper_2308_00763_b200.sharded import shard_layout
+
+    for K in (2048, 10_000, 300_007, 1 << 30):
+        for S in (2, 3, 4, 8):
+            try:
+                st, lay = shard_layout(K, S)
+            except ValueError:
+                with pytest.raises(ValueError):
+                    shard_tiles(K, S)
+                continue
+            assert st == shard_tiles(K, S)
+            assert st & (st - 1) == 0
+            assert sum(c for _, c in lay) == K and all(c > 0 for _, c in lay)
+            assert [f for f, _ in lay] == [r * st * 1024 for r in range(S)]

@@ -64,9 +64,9 @@ def main():
         rows.append(dict(
             entry=rel(fu[:, 0]), draws=rel(fu[:, 1]), release=rel(fu[:, 2]), window=rel(fu[:, 3]),
             parts=rel(fu[:, 4]), exit=rel(fu[:, 5]), t_entry=rel(tb[:, 0]), t_rel=rel(tb[:, 1]),
-            t_max=rel(tb[:, 4]), t_win=rel(tb[:, 5]), t_tree=rel(tb[:, 2]), t_end=rel(tb[:, 3]) if (tb[:, 3] > 0).any() else (0, 0), t0=t0))
+            t_max=rel(tb[:, 4]), t_scan=rel(tb[:, 6]), t_tab=rel(tb[:, 7]), t_win=rel(tb[:, 5]), t_tree=rel(tb[:, 2]), t_end=rel(tb[:, 3]) if (tb[:, 3] > 0).any() else (0, 0), t0=t0))
     print(f"{args.config} {prec} K={cfg['K']} tiles={nt} chunks={nc} frames={F}")
-    keys = ["entry", "draws", "release", "window", "parts", "exit", "t_entry", "t_rel", "t_max", "t_win", "t_tree", "t_end"]
+    keys = ["entry", "draws", "release", "window", "parts", "exit", "t_entry", "t_rel", "t_max", "t_scan", "t_tab", "t_win", "t_tree", "t_end"]
     med = {k: (np.median([r[k][0] for r in rows[1:]]), np.median([r[k][1] for r in rows[1:]])) for k in keys}
     for k in keys:
         print(f"  {k:8s} first {med[k][0]:8.2f} us   last {med[k][1]:8.2f} us")
