@@ -8,6 +8,7 @@
 #include <cuda_runtime.h>
 
 #include <climits>
+#include <cstdlib>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -201,6 +202,9 @@ struct pf_handle {
   unsigned long long* sh_gmax = nullptr;
   cudaEvent_t xev = nullptr;
   int sh_F = 0;
+  // unsharded track too large for the co-resident chunked table: run the
+  // sharded table kernels with one shard (no spinning across CTAs)
+  bool split_table = false;
   unsigned long long* d_trace = nullptr;  // pf_set_trace: [frame][n_tiles + n_chunks][8]
   size_t trace_cap = 0;
   bool tracing = false;
@@ -230,7 +234,8 @@ static cudaError_t set_fused_smem(const pf_handle* h) {
 // before its predecessor finishes and waits (griddepcontrol.wait) where it
 // consumes the predecessor's results
 template <typename Args>
-static cudaError_t launch_pdl(const pf_handle* h, const void* fn, dim3 grid, dim3 block, size_t smem, Args args) {
+static cudaError_t launch_pdl(const pf_handle* h, const void* fn, dim3 grid, dim3 block, size_t smem, Args args,
+                              bool allow = true) {
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = grid;
   cfg.blockDim = block;
@@ -238,7 +243,7 @@ static cudaError_t launch_pdl(const pf_handle* h, const void* fn, dim3 grid, dim
   cfg.stream = h->stream;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[0].val.programmaticStreamSerializationAllowed = h->pdl ? 1 : 0;
+  attr[0].val.programmaticStreamSerializationAllowed = (h->pdl && allow) ? 1 : 0;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   void* params[1] = {&args};
@@ -527,14 +532,35 @@ static int create_impl(pf_handle** out, const pf_config* cfg, int n_shards, int 
       ce = cudaFuncSetAttribute(pfk::pf_map_half, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->map_smem);
     CK(cudack(ce, "map smem attr"));
   }
-  if (n_shards > 1) {
+  if (n_shards == 1) {
+    // the chunked table exchanges through spinning CTAs: all of a frame's
+    // chunks must be co-resident, else the sharded kernels run it (1 shard)
+    int per_sm = 0, sms = 0;
+    const void* tk = h->km == 0 ? (const void*)pfk::pf_tile_table<0>
+                     : h->km == 1 ? (const void*)pfk::pf_tile_table<1> : (const void*)pfk::pf_tile_table<2>;
+    CK(cudack(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, tk, h->tpb_table, 0), "occupancy"));
+    CK(cudack(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, h->device), "attr"));
+    const char* force = std::getenv("PF_FORCE_SPLIT_TABLE");  // test knob: exercise the split path small
+    if ((long long)h->n_chunks * h->n_tracks > (long long)per_sm * sms / 2 ||
+        (force && force[0] == '1' && h->n_tracks == 1)) {
+      if (h->n_tracks != 1) {
+        e = "too many table chunks for co-residency with several tracks (split the batch)";
+        g_err = e;
+        pf_destroy(h);
+        return PF_EINVAL;
+      }
+      h->split_table = true;
+      h->sh_chunks = (h->nl + pfk::kShardChunk - 1) / pfk::kShardChunk;
+    }
+  }
+  if (n_shards > 1 || h->split_table) {
     CK(cudack(cudaMalloc(&h->sh_mass, (size_t)h->nl * 8), "shard"));
     CK(cudack(cudaMalloc(&h->sh_ctot, (size_t)h->sh_chunks * 8), "shard"));
     CK(cudack(cudaMalloc(&h->sh_croots, (size_t)h->sh_chunks * 3 * 8), "shard"));
     CK(cudack(cudaMalloc(&h->sh_send, 4 * 8), "shard"));
     CK(cudack(cudaMalloc(&h->sh_gsum, (size_t)n_shards * 4 * 8), "shard"));
     CK(cudack(cudaMalloc(&h->sh_gmax, (size_t)n_shards * 8), "shard"));
-    CK(cudack(cudaEventCreateWithFlags(&h->xev, cudaEventDisableTiming), "event"));
+    if (n_shards > 1) CK(cudack(cudaEventCreateWithFlags(&h->xev, cudaEventDisableTiming), "event"));
   }
   // own buffers as shard `shard`'s source pointers (peers are set later)
   void* own[8] = {h->X[0], h->X[1], h->C[0], h->C[1], h->tab_s, h->tab_O, h->tab_invM, h->win};
@@ -607,6 +633,8 @@ static int launch_maps(pf_handle* h, const uint8_t* dframes, int F) {
   return PF_OK;
 }
 
+static int shard_tables_launch(pf_handle* h, int traj_index, int traj_stride);
+
 // one frame: fused kernel + tile table
 static int launch_frame(pf_handle* h, const void* map_slot, long long map_video_stride, int traj_index,
                         int traj_stride) {
@@ -657,15 +685,25 @@ static int launch_frame(pf_handle* h, const void* map_slot, long long map_video_
   a.tt = h->tt;
   a.win = h->win;
   a.tmax = h->tsync;
-  // sharded frames are stream-ordered (collectives in between): no early release
-  a.ready_target = h->n_shards > 1 ? 0ULL : (unsigned long long)h->n_chunks * (unsigned long long)h->frame_counter;
+  // sharded / split-table frames are stream-ordered (no PDL, no early release)
+  const bool ordered = h->n_shards > 1 || h->split_table;
+  a.ready_target = ordered ? 0ULL : (unsigned long long)h->n_chunks * (unsigned long long)h->frame_counter;
   const size_t tr_frame = (size_t)(h->n_tiles + h->n_chunks) * 8;
   a.trace = (h->tracing && h->d_trace) ? h->d_trace + (size_t)traj_index * tr_frame : nullptr;
-  PF_CUDA(launch_pdl(h, (const void*)fused_kernel(h), dim3(h->nl, h->n_tracks), dim3(h->tpb), h->fused_smem, a),
+  PF_CUDA(launch_pdl(h, (const void*)fused_kernel(h), dim3(h->nl, h->n_tracks), dim3(h->tpb), h->fused_smem, a,
+                     !ordered),
           h->err);
   PF_CUDA(cudaGetLastError(), h->err);
   if (h->n_shards > 1) {  // the sharded tables run after the host's collectives (pf_shard_*)
     h->launches += 1;
+    return PF_OK;
+  }
+  if (h->split_table) {  // one shard: the exchanges are the shard's own buffers
+    int rc = shard_tables_launch(h, traj_index, traj_stride);
+    if (rc) return rc;
+    h->launches += 4;
+    h->cur = 1 - h->cur;
+    h->frame_counter += 1;
     return PF_OK;
   }
   if (h->profiling) PF_CUDA(cudaEventRecord(h->pev[3 * traj_index + 1], h->stream), h->err);
@@ -1021,9 +1059,33 @@ static pfk::ShardArgs shard_args(pf_handle* h, int f) {
   a.x0 = h->x0;
   a.traj = h->d_traj;
   a.traj_index = f;
+  if (h->n_shards == 1) {  // split table of an unsharded track: no exchange
+    a.gmax = h->tsync;
+    a.gsum = h->sh_send;
+  }
   a.degenerate = h->d_degen;
   a.t = (int)h->frame_counter;
   return a;
+}
+
+static int shard_tables_launch(pf_handle* h, int traj_index, int traj_stride) {
+  (void)traj_stride;  // one track
+  const pfk::ShardArgs a = shard_args(h, traj_index);
+  if (h->km == 0) {
+    pfk::pf_shard_mass<0><<<h->sh_chunks, pfk::kShardChunk, 0, h->stream>>>(a);
+    pfk::pf_shard_sum<0><<<1, 1024, 0, h->stream>>>(a);
+    pfk::pf_shard_finish<0><<<h->sh_chunks, pfk::kShardChunk, 0, h->stream>>>(a);
+  } else if (h->km == 1) {
+    pfk::pf_shard_mass<1><<<h->sh_chunks, pfk::kShardChunk, 0, h->stream>>>(a);
+    pfk::pf_shard_sum<1><<<1, 1024, 0, h->stream>>>(a);
+    pfk::pf_shard_finish<1><<<h->sh_chunks, pfk::kShardChunk, 0, h->stream>>>(a);
+  } else {
+    pfk::pf_shard_mass<2><<<h->sh_chunks, pfk::kShardChunk, 0, h->stream>>>(a);
+    pfk::pf_shard_sum<2><<<1, 1024, 0, h->stream>>>(a);
+    pfk::pf_shard_finish<2><<<h->sh_chunks, pfk::kShardChunk, 0, h->stream>>>(a);
+  }
+  PF_CUDA(cudaGetLastError(), h->err);
+  return PF_OK;
 }
 
 int pf_shard_tables(pf_handle* h) {

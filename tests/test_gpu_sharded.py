@@ -124,3 +124,15 @@ def test_two_processes_ipc_peer_reads(pf, mode, tmp_path):
     mp.spawn(_dist_worker, args=(2, _free_port(), K, mode, str(tmp_path)), nprocs=2, join=True)
     for r in range(2):
         assert np.array_equal(np.load(tmp_path / f"traj{r}.npy"), one)
+
+
+@pytest.mark.parametrize("mode", ["fp64", "fp16"])
+@pytest.mark.parametrize("K", [10_000, 2_000_000])
+def test_split_table_equals_chunked(pf, mode, K, monkeypatch):
+    # tracks too large for the co-resident chunked table (2^30 on one GPU) run
+    # the sharded table kernels with one shard; forced here at small K
+    frames, _ = rp.generate_video(rp.Params(), 6, 96, 80, (40.0, 30.0), 17)
+    one = pf.Filter(K, mode, 96, 80, 5, start_hint=(40.0, 30.0)).run(frames)
+    monkeypatch.setenv("PF_FORCE_SPLIT_TABLE", "1")
+    two = pf.Filter(K, mode, 96, 80, 5, start_hint=(40.0, 30.0)).run(frames)
+    assert np.array_equal(one, two)
