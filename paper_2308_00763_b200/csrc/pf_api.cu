@@ -223,7 +223,14 @@ static fused_fn fused_for_tpb(int tpb) {
     default: return pfk::pf_fused_frame<M, 4, 1>;
   }
 }
+// sharded filters: 128 or 256 threads per block only (keeps the instantiations few)
+template <int M>
+static fused_fn fused_sharded(int tpb) {
+  return tpb == 128 ? pfk::pf_fused_frame<M, 8, 1, true> : pfk::pf_fused_frame<M, 4, 1, true>;
+}
 static fused_fn fused_kernel(const pf_handle* h) {
+  if (h->n_shards > 1)
+    return h->km == 0 ? fused_sharded<0>(h->tpb) : h->km == 1 ? fused_sharded<1>(h->tpb) : fused_sharded<2>(h->tpb);
   return h->km == 0 ? fused_for_tpb<0>(h->tpb) : h->km == 1 ? fused_for_tpb<1>(h->tpb) : fused_for_tpb<2>(h->tpb);
 }
 static cudaError_t set_fused_smem(const pf_handle* h) {
@@ -372,6 +379,7 @@ static int create_impl(pf_handle** out, const pf_config* cfg, int n_shards, int 
     const long long ctas = ((cfg->K + PF_TILE - 1) / PF_TILE) * (long long)cfg->n_tracks;
     h->tpb = cfg->tpb ? cfg->tpb : (cfg->precision >= PF_FP16 && ctas <= 2048 ? 128 : 256);
   }
+  if (n_shards > 1 && h->tpb != 128) h->tpb = 256;  // sharded kernels exist for 128 / 256 threads
   h->vpt = h->tpb >= 1024 ? 1 : h->tpb >= 512 ? 2 : h->tpb >= 256 ? 4 : 8;
   h->params = cfg->params;
   h->n_off = cfg->n_offsets;
@@ -487,16 +495,16 @@ static int create_impl(pf_handle** out, const pf_config* cfg, int n_shards, int 
   build_exp16(ex.data());
   CK(cudack(cudaMalloc(&h->exp16, 65536 * 2), "exp16"));
   CK(cudack(cudaMemcpy(h->exp16, ex.data(), 65536 * 2, cudaMemcpyHostToDevice), "exp16"));
-  // ziggurat fast-path tables, packed for 16-byte smem staging
+  // ziggurat fast-path tables, packed for 16-byte smem staging: 256 x (ki >> 20) then 256 x wi
   {
-    std::vector<unsigned char> zt(3072);
+    std::vector<unsigned char> zt(pfk::kZigBytes);
     for (int i = 0; i < 256; ++i) {
       uint32_t khi = (uint32_t)(PF_ZIG_KI_HOST[i] >> 20);
       std::memcpy(zt.data() + 4 * i, &khi, 4);
       std::memcpy(zt.data() + 1024 + 8 * i, &PF_ZIG_WI_BITS_HOST[i], 8);
     }
-    CK(cudack(cudaMalloc(&h->zig, 3072), "zig"));
-    CK(cudack(cudaMemcpy(h->zig, zt.data(), 3072, cudaMemcpyHostToDevice), "zig"));
+    CK(cudack(cudaMalloc(&h->zig, pfk::kZigBytes), "zig"));
+    CK(cudack(cudaMemcpy(h->zig, zt.data(), pfk::kZigBytes, cudaMemcpyHostToDevice), "zig"));
   }
   // template + pairwise plan
   std::vector<int2> offs(h->n_off);

@@ -22,8 +22,13 @@
 #include "pf_math.cuh"
 #include "pf_rng.cuh"
 
+#include <type_traits>
+
 #define PF_TILE 1024
 #define PF_MAX_SHARDS 8
+#ifndef PF_FULL_SPEC
+#define PF_FULL_SPEC 1  // full-tile threads take a bounds-free phase-1 path
+#endif
 #define PF_XQ_BITS 10
 
 namespace pfk {
@@ -627,6 +632,11 @@ constexpr int max_src_tiles() {  // source tiles staged in shared memory (else g
 // memory -- was measured: slightly better latency at C2, worse at C3/C4 since
 // it copies every source position, not only the ancestors; not done)
 
+// ziggurat fast-path tables in shared memory: 256 x (ki >> 20) then 256 x wi
+// (a 512-entry signed {wi, ki} table was measured: fewer instructions, but the
+// 8 KB per-CTA staging and 16-byte random reads made C2 / C3 slower)
+constexpr int kZigBytes = 3072;
+
 constexpr int kSlowQ = 128;  // deferred ziggurat slow paths per CTA (overflow -> inline)
 
 // shared-memory footprint: ziggurat tables, noise/positions (vec per particle),
@@ -635,7 +645,7 @@ template <int MODE>
 constexpr size_t fused_smem_bytes() {
   using real = typename Tr<MODE>::real;
   using vec = typename Tr<MODE>::vec;
-  return 3072 + PF_TILE * sizeof(vec) + max_src_tiles<MODE>() * PF_TILE * sizeof(real) + 16 +
+  return kZigBytes + PF_TILE * sizeof(vec) + max_src_tiles<MODE>() * PF_TILE * sizeof(real) + 16 +
          (max_src_tiles<MODE>() + 1) * 24 + kSlowQ * 12 + 320 * 8;
 }
 
@@ -720,7 +730,7 @@ __device__ __forceinline__ double tree_vpt(const double* v) {
 
 // One CTA = one tile of PF_TILE particles of one track; TPB = PF_TILE/(VPT*R)
 // threads, thread t of round r owns particles (r*TPB + t)*VPT .. +VPT-1.
-template <int MODE, int VPT, int R>
+template <int MODE, int VPT, int R, bool SH = false>  // SH: sharded filter (source tiles on several shards)
 __global__ void __launch_bounds__(PF_TILE / (VPT * R)) pf_fused_frame(FusedArgs a) {
   using real = typename Tr<MODE>::real;
   using vec = typename Tr<MODE>::vec;
@@ -730,10 +740,10 @@ __global__ void __launch_bounds__(PF_TILE / (VPT * R)) pf_fused_frame(FusedArgs 
   constexpr int TPB = PF_TILE / (VPT * R);
   constexpr int NW = TPB / 32;
   extern __shared__ __align__(16) unsigned char smem[];
-  uint32_t* s_kihi = reinterpret_cast<uint32_t*>(smem);   // 1 KB
-  double* s_wi = reinterpret_cast<double*>(smem + 1024);  // 2 KB
-  vec* s_X = reinterpret_cast<vec*>(smem + 3072);  // per-particle noise
-  real* s_c = reinterpret_cast<real*>(smem + 3072 + PF_TILE * sizeof(vec));
+  const uint32_t* s_kihi = reinterpret_cast<const uint32_t*>(smem);    // 1 KB
+  const double* s_wi = reinterpret_cast<const double*>(smem + 1024);  // 2 KB
+  vec* s_X = reinterpret_cast<vec*>(smem + kZigBytes);                // per-particle scaled noise
+  real* s_c = reinterpret_cast<real*>(smem + kZigBytes + PF_TILE * sizeof(vec));
   unsigned char* p_tab = reinterpret_cast<unsigned char*>(s_c + MS * PF_TILE);
   int* s_ts = reinterpret_cast<int*>(p_tab);                        // MS + 1 (in-track indices)
   double* s_tO = reinterpret_cast<double*>(p_tab + (MS + 1) * 8);   // MS + 1
@@ -760,7 +770,7 @@ __global__ void __launch_bounds__(PF_TILE / (VPT * R)) pf_fused_frame(FusedArgs 
   const real* __restrict__ map = reinterpret_cast<const real*>(a.map) + (size_t)(track % a.n_videos) * a.map_video_stride;
   // source tile b (global) -> (shard, local tile); track offsets apply when unsharded
   auto shard_of = [&](int b, int& lb) -> int {
-    if (a.src.n_shards == 1) {
+    if (!SH) {
       lb = b;
       return 0;
     }
@@ -768,10 +778,13 @@ __global__ void __launch_bounds__(PF_TILE / (VPT * R)) pf_fused_frame(FusedArgs 
     lb = b - sh * a.src.shard_tiles;
     return sh;
   };
-  auto src_X = [&](int b) -> const vec* {
-    int lb;
-    const int sh = shard_of(b, lb);
-    return reinterpret_cast<const vec*>(a.src.X[sh]) + (size_t)track * Kl + (size_t)lb * PF_TILE;
+  // position of global particle k (its shard's buffer; one IMAD when unsharded)
+  const vec* X0 = reinterpret_cast<const vec*>(a.src.X[0]) + (size_t)track * Kl;
+  const int shard_parts = a.src.shard_tiles * PF_TILE;
+  auto src_pos = [&](int k) -> const vec* {
+    if (!SH) return X0 + k;
+    const int sh = k / shard_parts;
+    return reinterpret_cast<const vec*>(a.src.X[sh]) + (k - sh * shard_parts);
   };
   auto src_C = [&](int b) -> const real* {
     int lb;
@@ -797,7 +810,7 @@ __global__ void __launch_bounds__(PF_TILE / (VPT * R)) pf_fused_frame(FusedArgs 
   {
     const uint4* zsrc = reinterpret_cast<const uint4*>(a.zig);
     uint4* zdst = reinterpret_cast<uint4*>(smem);
-    for (int i = tid; i < 192; i += TPB) zdst[i] = zsrc[i];
+    for (int i = tid; i < kZigBytes / 16; i += TPB) zdst[i] = zsrc[i];
   }
   PF_TRACE(a, 0);
   if (tid == 0) s_int[3] = 0;
@@ -838,15 +851,18 @@ __global__ void __launch_bounds__(PF_TILE / (VPT * R)) pf_fused_frame(FusedArgs 
         const unsigned long long w = xs;
         xs = pfr::kA * xs + pfr::kC;
         const unsigned whi = (unsigned)(w >> 32), wlo = (unsigned)w;
-        const unsigned idx = whi >> 24;
+        // layer (bits 56..63) and sign (bit 55) select a signed table entry:
+        // rabs * (-wi) == -(rabs * wi) exactly
         // rabs = bits 3..54 of w; (double)rabs exactly via the 2^52 bias trick
         const unsigned rlo = __funnelshift_r(wlo, whi, 3);
         const unsigned rhi = (whi >> 3) & 0xfffffu;
         const double rabs_d = __dsub_rn(__hiloint2double(0x43300000 | rhi, rlo), 4503599627370496.0);
+        const unsigned idx = whi >> 24;  // layer: bits 56..63
         const double x = __dmul_rn(rabs_d, s_wi[idx]);
         // sign (bit 55) flips the sign bit of the product
         nn[c] = __hiloint2double(__double2hiint(x) ^ ((whi << 8) & 0x80000000u), __double2loint(x));
-        slow |= (((rhi << 12) | (rlo >> 20)) >= s_kihi[idx] ? 1u : 0u) << (2 * i + c);
+        // fast-path test rabs < ki on the top 32 bits of rabs (bits 23..54 of w)
+        slow |= (__funnelshift_r(wlo, whi, 23) >= s_kihi[idx] ? 1u : 0u) << (2 * i + c);
       }
       s_X[l0 + i] = scale_noise<MODE>(to_vec<MODE>(nn[0], nn[1]), stdv);
     }
@@ -898,7 +914,21 @@ __global__ void __launch_bounds__(PF_TILE / (VPT * R)) pf_fused_frame(FusedArgs 
       const int2 wn = __ldcg(reinterpret_cast<const int2*>(a.win) + (size_t)track * nl + ltile);
       const int nsrc = wn.y - wn.x + 1;
       const int staged = nsrc <= MS ? 1 : 0;
-      if (staged && bulk_ok) {
+      if (!SH && staged && bulk_ok && lane == 0) {  // the window is contiguous: one bulk copy
+        const uint32_t bb = smem_u32(s_bar);
+        const int c0 = wn.x * PF_TILE;
+        const int cnt = min((wn.y + 1) * PF_TILE, K) - c0;
+        const uint32_t bytes = (uint32_t)((cnt * (int)sizeof(real) + 15) & ~15);  // C buffers carry 16 B of slack
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bb), "r"(1) : "memory");
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bb), "r"(bytes) : "memory");
+        asm volatile(
+            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                smem_u32(s_c)),
+            "l"(src_C(wn.x)), "r"(bytes), "r"(bb)
+            : "memory");
+      }
+      if (SH && staged && bulk_ok) {
         // one bulk copy per source tile (tiles may live on different shards)
         const uint32_t bb = smem_u32(s_bar);
         if (lane == 0) {
@@ -977,119 +1007,116 @@ __global__ void __launch_bounds__(PF_TILE / (VPT * R)) pf_fused_frame(FusedArgs 
   auto tile_C = [&](int b) -> const real* { return staged ? s_c + (b - b_lo) * PF_TILE : src_C(b); };
 
   // ---- phase 1: resample + propagate + likelihood -------------------------
+  // Threads whose VPT particles all lie inside the tile (all but at most one
+  // warp of the last tile) take the FULL path, free of per-particle bounds.
   real Lr[R][VPT];
   vec Xr[R][VPT];
   real tmax = neg_inf<MODE>();
+  const int mlo = -a.r, mhx = a.W - 1 + a.r, mhy = a.H - 1 + a.r;
+  const real* __restrict__ mapc = map + a.r * a.Wm + a.r;  // map origin at (x, y) = (0, 0)
+  const int Wm = a.Wm;
 #pragma unroll
   for (int rr = 0; rr < R; ++rr) {
     const int l0 = (rr * TPB + tid) * VPT;
-    int anc[VPT];          // global ancestor index
-    const vec* asrc[VPT];  // its position (in its shard's buffer)
-    if (a.t == 0 || l0 >= Tb) {  // frame 0: identity ancestors (own shard)
+    auto body = [&](auto full_tag) {
+      constexpr bool FULL = decltype(full_tag)::value;
+      auto in_tile = [&](int i) -> bool { return FULL || l0 + i < Tb; };
+      int anc[VPT];  // global ancestor index
+      if (a.t == 0 || (!FULL && l0 >= Tb)) {  // frame 0: identity ancestors
+#pragma unroll
+        for (int i = 0; i < VPT; ++i) anc[i] = base + l0 + i;
+      } else {
+        int b = b_lo;
+        if (!staged) {
+          int lo = b_lo, hi = b_hi;
+          while (lo < hi) {
+            const int mid = (lo + hi + 1) >> 1;
+            if (g_ts(mid) <= base + l0)
+              lo = mid;
+            else
+              hi = mid - 1;
+          }
+          b = lo;
+        }
+        // register-cached geometry of the current source tile
+        int sb = tab_s(b), snext = b < b_hi ? tab_s(b + 1) : K;
+        double gO = tab_O(b), gM = tab_M(b);
+        float fO = (float)gO, fM = (float)gM;  // FP16: the table holds f32 values
+        int tl = b * PF_TILE, tb = min(PF_TILE, K - tl);
+        const real* cb = tile_C(b);
+        int jprev = -1;
+#pragma unroll
+        for (int i = 0; i < VPT; ++i) {
+          const int k = base + l0 + i;
+          if (!FULL && k >= K) {
+            anc[i] = k;
+            continue;
+          }
+          if (k >= snext) {  // next source tile (rare: outputs of one source tile are contiguous)
+            do {
+              ++b;
+              snext = b < b_hi ? tab_s(b + 1) : K;
+            } while (k >= snext);
+            sb = tab_s(b);
+            gO = tab_O(b);
+            gM = tab_M(b);
+            fO = (float)gO;
+            fM = (float)gM;
+            tl = b * PF_TILE;
+            tb = min(PF_TILE, K - tl);
+            cb = tile_C(b);
+            jprev = -1;
+          }
+          typename KT::k_t kq;
+          if constexpr (MODE == M_FP16) {
+            // f32 tile-local point: q = ((k - s_b) + phi_b) * rho_b
+            const float qf = __fmul_rn(__fadd_rn((float)(k - sb), fO), fM);
+            kq = __half_as_ushort(__float2half_ru(fminf(fmaxf(qf, 0.0f), 1.0f)));
+          } else {
+            const double p = point_of<MODE>(k, u, K, invK);
+            const double q = gM == 0.0 ? 0.0 : __dmul_rn(__dsub_rn(p, gO), gM);
+            kq = KT::up(fmin(fmax(q, 0.0), 1.0));
+          }
+          int j = jprev >= 0 ? advance_key<MODE>(cb, jprev, tb, kq) : lb_branchless<MODE>(cb, tb, kq);
+          j = min(j, tb - 1);
+          jprev = j;
+          anc[i] = tl + j;
+        }
+      }
+      if (a.dbg_anc != nullptr) {
+#pragma unroll
+        for (int i = 0; i < VPT; ++i)
+          if (in_tile(i)) a.dbg_anc[(size_t)track * Kl + lbase + l0 + i] = anc[i];
+      }
+      // all VPT ancestor gathers first (independent, read-only X_prev), then
+      // propagation and all VPT map lookups, then the new positions' stores --
+      // no store sits between loads, so nothing serialises the memory latency
+      vec xa[VPT];
 #pragma unroll
       for (int i = 0; i < VPT; ++i) {
-        anc[i] = base + l0 + i;
-        asrc[i] = reinterpret_cast<const vec*>(a.src.X[a.src.n_shards == 1 ? 0 : tile / a.src.shard_tiles]) +
-                  (size_t)track * Kl + lbase + l0 + i;
-      }
-    } else {
-      int b = b_lo;
-      if (!staged) {
-        int lo = b_lo, hi = b_hi;
-        while (lo < hi) {
-          const int mid = (lo + hi + 1) >> 1;
-          if (g_ts(mid) <= base + l0)
-            lo = mid;
-          else
-            hi = mid - 1;
-        }
-        b = lo;
-      }
-      // register-cached geometry of the current source tile
-      int sb = tab_s(b), snext = b < b_hi ? tab_s(b + 1) : K;
-      double gO = tab_O(b), gM = tab_M(b);
-      float fO = (float)gO, fM = (float)gM;  // FP16: the table holds f32 values
-      int tl = b * PF_TILE, tb = min(PF_TILE, K - tl);
-      const real* cb = tile_C(b);
-      const vec* xb = src_X(b);
-      int jprev = -1;
-#pragma unroll
-      for (int i = 0; i < VPT; ++i) {
-        const int k = base + l0 + i;
-        if (k >= K) {
-          anc[i] = k;
-          asrc[i] = xb;
-          continue;
-        }
-        if (k >= snext) {  // next source tile (rare: outputs of one source tile are contiguous)
-          do {
-            ++b;
-            snext = b < b_hi ? tab_s(b + 1) : K;
-          } while (k >= snext);
-          sb = tab_s(b);
-          gO = tab_O(b);
-          gM = tab_M(b);
-          fO = (float)gO;
-          fM = (float)gM;
-          tl = b * PF_TILE;
-          tb = min(PF_TILE, K - tl);
-          cb = tile_C(b);
-          xb = src_X(b);
-          jprev = -1;
-        }
-        typename KT::k_t kq;
-        if constexpr (MODE == M_FP16) {
-          // f32 tile-local point: q = ((k - s_b) + phi_b) * rho_b
-          const float qf = __fmul_rn(__fadd_rn((float)(k - sb), fO), fM);
-          kq = __half_as_ushort(__float2half_ru(fminf(fmaxf(qf, 0.0f), 1.0f)));
+        if (in_tile(i)) {
+          xa[i] = __ldg(src_pos(anc[i]));
         } else {
-          const double p = point_of<MODE>(k, u, K, invK);
-          const double q = gM == 0.0 ? 0.0 : __dmul_rn(__dsub_rn(p, gO), gM);
-          kq = KT::up(fmin(fmax(q, 0.0), 1.0));
+          xa[i].x = (real)0;
+          xa[i].y = (real)0;
         }
-        int j = jprev >= 0 ? advance_key<MODE>(cb, jprev, tb, kq) : lb_branchless<MODE>(cb, tb, kq);
-        j = min(j, tb - 1);
-        jprev = j;
-        anc[i] = tl + j;
-        asrc[i] = xb + j;
       }
-    }
-    if (a.dbg_anc != nullptr) {
 #pragma unroll
-      for (int i = 0; i < VPT; ++i)
-        if (l0 + i < Tb) a.dbg_anc[(size_t)track * Kl + lbase + l0 + i] = anc[i];
-    }
-    // all VPT ancestor gathers first (independent, read-only X_prev), then
-    // propagation and all VPT map lookups, then the new positions' stores --
-    // no store sits between loads, so nothing serialises the memory latency
-    vec xa[VPT];
-#pragma unroll
-    for (int i = 0; i < VPT; ++i) {
-      if (l0 + i < Tb) {
-        xa[i] = __ldg(asrc[i]);
-      } else {
-        xa[i].x = (real)0;
-        xa[i].y = (real)0;
+      for (int i = 0; i < VPT; ++i) {
+        if (in_tile(i)) {
+          const vec xn = prop<MODE>(xa[i], s_X[l0 + i], drift);
+          const int ix = round_clamp<MODE>(xn.x, mlo, mhx);
+          const int iy = round_clamp<MODE>(xn.y, mlo, mhy);
+          Lr[rr][i] = __ldg(mapc + iy * Wm + ix);
+          Xr[rr][i] = xn;
+        } else {  // outside the tile: weight exp(-inf) = 0, position 0
+          Lr[rr][i] = neg_inf<MODE>();
+          Xr[rr][i].x = (real)0;
+          Xr[rr][i].y = (real)0;
+        }
       }
-    }
-#pragma unroll
-    for (int i = 0; i < VPT; ++i) {
-      const int l = l0 + i;
-      if (l < Tb) {
-        const vec xn = prop<MODE>(xa[i], s_X[l], drift);
-        const int ix = round_clamp<MODE>(xn.x, -a.r, a.W - 1 + a.r);
-        const int iy = round_clamp<MODE>(xn.y, -a.r, a.H - 1 + a.r);
-        Lr[rr][i] = __ldg(map + (iy + a.r) * a.Wm + (ix + a.r));
-        Xr[rr][i] = xn;
-      } else {
-        Lr[rr][i] = neg_inf<MODE>();
-        Xr[rr][i].x = (real)0;
-        Xr[rr][i].y = (real)0;
-      }
-    }
-    {
       constexpr int VB = VPT * (int)sizeof(vec);
-      if (VB % 16 == 0 && l0 + VPT <= Tb && ((((size_t)track * Kl) * sizeof(vec)) % 16) == 0) {
+      if (VB % 16 == 0 && (FULL || l0 + VPT <= Tb) && ((((size_t)track * Kl) * sizeof(vec)) % 16) == 0) {
         uint4* dst = reinterpret_cast<uint4*>(Xn + lbase + l0);
 #pragma unroll
         for (int q = 0; q < VB / 16; ++q) {
@@ -1100,12 +1127,18 @@ __global__ void __launch_bounds__(PF_TILE / (VPT * R)) pf_fused_frame(FusedArgs 
       } else {
 #pragma unroll
         for (int i = 0; i < VPT; ++i)
-          if (l0 + i < Tb) Xn[lbase + l0 + i] = Xr[rr][i];
+          if (in_tile(i)) Xn[lbase + l0 + i] = Xr[rr][i];
       }
-    }
 #pragma unroll
-    for (int i = 0; i < VPT; ++i)
-      if (gt_real<MODE>(Lr[rr][i], tmax)) tmax = Lr[rr][i];
+      for (int i = 0; i < VPT; ++i)
+        if (gt_real<MODE>(Lr[rr][i], tmax)) tmax = Lr[rr][i];
+    };
+#if PF_FULL_SPEC
+    if (l0 + VPT <= Tb)
+      body(std::true_type{});
+    else
+#endif
+      body(std::false_type{});
   }
   if (a.dbg_anc != nullptr) {  // debug capture (parity tests): recompute-free copies
 #pragma unroll
@@ -1144,7 +1177,7 @@ __global__ void __launch_bounds__(PF_TILE / (VPT * R)) pf_fused_frame(FusedArgs 
     double px[VPT], py[VPT];
 #pragma unroll
     for (int i = 0; i < VPT; ++i) {
-      const wq_t w = (l0 + i < Tb) ? weight_q<MODE>(Lr[rr][i], mtile, a.exp16) : (wq_t)0;
+      const wq_t w = weight_q<MODE>(Lr[rr][i], mtile, a.exp16);  // 0 outside the tile (L = -inf)
       run += w;
       cum[rr][i] = run;  // thread-local inclusive
       if constexpr (MODE == M_FP16) {
