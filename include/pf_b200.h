@@ -91,6 +91,12 @@ int pf_step(pf_handle* h, const uint8_t* frame, int32_t frame_on_device, double*
 
 int pf_degenerate_frame(const pf_handle* h);
 
+/* Debug/parity: the per-frame likelihood maps of F host frames (one video),
+ * [F][H+2r][W+2r] in the mode dtype (fp16 as uint16 bits): entry (iy+r, ix+r)
+ * is the reference likelihood of a particle at rint position (ix, iy),
+ * filter.py:204-217 (wide) / 384-423 (binary16). */
+int pf_likelihood_maps(pf_handle* h, const uint8_t* frames, int32_t n_frames, void* maps_out);
+
 /* Device-event timings of the last pf_run/pf_step, milliseconds:
  * [0] total, [1] upload, [2] likelihood maps, [3] fused frame kernels,
  * [4] tile tables, [5] download. */

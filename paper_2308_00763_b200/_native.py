@@ -63,6 +63,7 @@ SIGNATURES = [
     ("pf_run", C.c_int, [_VP, _VP, C.c_int32, C.c_int32, _VP]),
     ("pf_step", C.c_int, [_VP, _VP, C.c_int32, _VP]),
     ("pf_degenerate_frame", C.c_int, [_VP]),
+    ("pf_likelihood_maps", C.c_int, [_VP, _VP, C.c_int32, _VP]),
     ("pf_set_profiling", C.c_int, [_VP, C.c_int32]),
     ("pf_last_timings", C.c_int, [_VP, C.POINTER(C.c_float)]),
     ("pf_last_launches", C.c_int64, [_VP]),

@@ -183,6 +183,7 @@ struct pf_handle {
   int degenerate_frame = -1;
   size_t map_smem = 0, fused_smem = 0;
   int map_band = 32;
+  bool map_img = false;  // binary16 term-image map kernel
   bool profiling = false;
   std::vector<cudaEvent_t> pev;  // 3 per frame when profiling
   bool use_graphs = true;
@@ -530,6 +531,16 @@ static int create_impl(pf_handle** out, const pf_config* cfg, int n_shards, int 
   h->fused_smem = h->km == 0 ? pfk::fused_smem_bytes<0>() : h->km == 1 ? pfk::fused_smem_bytes<1>()
                                                                       : pfk::fused_smem_bytes<2>();
   CK(cudack(set_fused_smem(h), "fused smem attr"));
+  // binary16: the term-image kernel when its shared memory fits
+  h->map_img = false;
+  if (h->km == 2) {
+    const pfk::MapHalfGeom g = pfk::map_half_geom(h->W, h->H, h->r, h->n_off);
+    if (g.smem <= 200 * 1024) {
+      h->map_img = true;
+      CK(cudack(cudaFuncSetAttribute(pfk::pf_map_half_img, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)g.smem),
+                "map smem attr"));
+    }
+  }
   if (h->map_smem > 48 * 1024) {
     cudaError_t ce = cudaSuccess;
     if (h->km == 0)
@@ -634,7 +645,11 @@ static int launch_maps(pf_handle* h, const uint8_t* dframes, int F) {
     pfk::pf_map_wide<double><<<grid, 256, h->map_smem, h->stream>>>(a);
   else if (h->km == 1)
     pfk::pf_map_wide<float><<<grid, 256, h->map_smem, h->stream>>>(a);
-  else
+  else if (h->map_img) {
+    const pfk::MapHalfGeom g = pfk::map_half_geom(h->W, h->H, h->r, h->n_off);
+    dim3 gi((h->Hm + g.band - 1) / g.band, h->n_videos * F);
+    pfk::pf_map_half_img<<<gi, pfk::kMapHalfThreads, g.smem, h->stream>>>(a);
+  } else
     pfk::pf_map_half<<<grid, 256, h->map_smem, h->stream>>>(a);
   h->launches += 1;
   PF_CUDA(cudaGetLastError(), h->err);
@@ -872,6 +887,22 @@ int pf_run(pf_handle* h, const uint8_t* frames, int32_t F, int32_t on_device, do
   cudaEventElapsedTime(&ms, h->ev[3], h->ev[4]);
   h->timings[5] = ms;
   return finish_degenerate(h);
+}
+
+int pf_likelihood_maps(pf_handle* h, const uint8_t* frames, int32_t F, void* maps_out) {
+  if (!h || !frames || F < 1 || !maps_out || h->n_videos != 1) return PF_EINVAL;
+  PF_CUDA(cudaSetDevice(h->device), h->err);
+  const size_t fbytes = (size_t)F * h->H * h->W;
+  const size_t mbytes = (size_t)F * h->Hm * h->Wm * h->rs;
+  int rc;
+  if ((rc = grow((void**)&h->d_frames, &h->frames_cap, fbytes, h->err))) return rc;
+  if ((rc = grow((void**)&h->d_maps, &h->maps_cap, mbytes, h->err))) return rc;
+  h->g_F = -1;  // the map buffer may have moved: re-capture the frame graph
+  PF_CUDA(cudaMemcpyAsync(h->d_frames, frames, fbytes, cudaMemcpyHostToDevice, h->stream), h->err);
+  if ((rc = launch_maps(h, h->d_frames, F))) return rc;
+  PF_CUDA(cudaMemcpyAsync(maps_out, h->d_maps, mbytes, cudaMemcpyDeviceToHost, h->stream), h->err);
+  PF_CUDA(cudaStreamSynchronize(h->stream), h->err);
+  return PF_OK;
 }
 
 int pf_step(pf_handle* h, const uint8_t* frame, int32_t on_device, double* est_out) {

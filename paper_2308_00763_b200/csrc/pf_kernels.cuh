@@ -265,6 +265,118 @@ __global__ void pf_map_half(MapArgs a) {
   }
 }
 
+// binary16 map, term-image formulation (used when its shared memory fits):
+// the CTA's band of map rows reads a padded image T[py][px] = term16(frame
+// pixel, edge-clamped) held twice -- A and B = A shifted by one half -- so
+// every tap of every entry pair is ONE aligned 32-bit shared load (A for even,
+// B for odd tap offsets, a warp-uniform choice) feeding one HADD2: per entry
+// pair and tap, LDS + IADD + HADD2 instead of two clamped pixel and term
+// lookups.  Same per-entry fold (template order from +0, each add RN16), so
+// the map is bit-identical to pf_map_half.
+constexpr int kMapHalfThreads = 512;
+constexpr int kMapHalfPairs = 8;  // entry pairs per thread (<= 4096 per CTA)
+struct MapHalfGeom {
+  int band, P, rows_img;  // map rows per CTA, image pitch (halves, even), image rows
+  size_t smem;            // dynamic shared memory bytes
+};
+__host__ __device__ inline MapHalfGeom map_half_geom(int W, int H, int r, int n_off) {
+  MapHalfGeom g;
+  const int Wm = W + 2 * r, Hm = H + 2 * r, npr = (Wm + 1) / 2;
+  g.band = max(1, min(Hm, kMapHalfThreads * kMapHalfPairs / npr));
+  g.P = (Wm + 2 * r + 2) & ~1;
+  g.rows_img = g.band + 2 * r;
+  const size_t frame_rows = (size_t)(g.band + 2 * r) * W + 32;
+  g.smem = 16 + 256 * 2 + (size_t)n_off * 4 + 16 + ((frame_rows + 15) & ~(size_t)15) + (size_t)2 * g.rows_img * g.P * 2;
+  return g;
+}
+
+__global__ void __launch_bounds__(kMapHalfThreads) pf_map_half_img(MapArgs a) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const MapHalfGeom g = map_half_geom(a.W, a.H, a.r, a.n_off);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem);
+  __half* term = reinterpret_cast<__half*>(smem + 16);
+  int* tapw = reinterpret_cast<int*>(smem + 16 + 512);
+  uint8_t* rows = reinterpret_cast<uint8_t*>(((uintptr_t)(tapw + a.n_off) + 15) & ~(uintptr_t)15);
+  const size_t frame_rows = (size_t)(g.band + 2 * a.r) * a.W + 32;
+  __half* imgA = reinterpret_cast<__half*>(rows + ((frame_rows + 15) & ~(size_t)15));
+  __half* imgB = imgA + (size_t)g.rows_img * g.P;
+  const unsigned* wA = reinterpret_cast<const unsigned*>(imgA);
+
+  const int vf = blockIdx.y;
+  const int my0 = blockIdx.x * g.band;
+  const int my1 = min(a.Hm, my0 + g.band);
+  const int R0 = max(0, my0 - 2 * a.r);
+  const int R1 = min(a.H - 1, my1 - 1);
+  const uint8_t* frame = a.frames + (size_t)vf * a.H * a.W;
+
+  const __half bg = __ushort_as_half(a.bg16), fg = __ushort_as_half(a.fg16), s = __ushort_as_half(a.s16);
+  for (int i = threadIdx.x; i < 256; i += blockDim.x) {  // model.half_term_stabilized, 7 RN16 ops
+    __half v = __int2half_rn(i);
+    __half x = __hmul_rn(__hsub_rn(v, bg), s);
+    __half x2 = __hmul_rn(x, x);
+    __half y = __hmul_rn(__hsub_rn(v, fg), s);
+    __half y2 = __hmul_rn(y, y);
+    term[i] = __hsub_rn(x2, y2);
+  }
+  // tap offsets in 32-bit words from imgA: (dy + r) * P + (dx + r) halves,
+  // odd offsets read B (its word w holds A halves 2w + 1, 2w + 2)
+  const int bwords = g.rows_img * g.P / 2;
+  for (int j = threadIdx.x; j < a.n_off; j += blockDim.x) {
+    const int2 o = a.offsets[j];
+    const int t = (o.y + a.r) * g.P + (o.x + a.r);
+    tapw[j] = (t >> 1) + ((t & 1) ? bwords : 0);
+  }
+  const int nrows = R1 >= R0 ? R1 - R0 + 1 : 0;
+  const uint32_t bytes = (uint32_t)nrows * (uint32_t)a.W;
+  const uint8_t* src = frame + (size_t)R0 * a.W;
+  if (nrows > 0 && ((uintptr_t)src % 16 == 0) && (bytes % 16 == 0)) {
+    bulk_load_rows(rows, src, bytes, bar);
+  } else {
+    for (uint32_t i = threadIdx.x; i < bytes; i += blockDim.x) rows[i] = src[i];
+  }
+  __syncthreads();
+  // padded term images: row py <-> frame row clamp(my0 + py - 2r), column px <-> clamp(px - 2r)
+  for (int i = threadIdx.x; i < g.rows_img * g.P; i += blockDim.x) {
+    const int py = i / g.P, px = i - py * g.P;
+    const int y = min(max(my0 + py - 2 * a.r, 0), a.H - 1);
+    const uint8_t* row = rows + (max(y, R0) - R0) * a.W;
+    const int x0 = min(max(px - 2 * a.r, 0), a.W - 1), x1 = min(max(px + 1 - 2 * a.r, 0), a.W - 1);
+    imgA[i] = term[row[x0]];
+    imgB[i] = term[row[x1]];
+  }
+  __syncthreads();
+
+  const int npr = (a.Wm + 1) / 2, npairs = (my1 - my0) * npr;
+  int base[kMapHalfPairs];
+  __half2 acc[kMapHalfPairs];
+#pragma unroll
+  for (int k = 0; k < kMapHalfPairs; ++k) {
+    const int p = min(threadIdx.x + k * kMapHalfThreads, max(npairs - 1, 0));
+    const int row = p / npr, x2 = p - row * npr;
+    base[k] = row * (g.P / 2) + x2;
+    acc[k] = __float2half2_rn(0.0f);
+  }
+  for (int j = 0; j < a.n_off; ++j) {
+    const int tw = tapw[j];
+#pragma unroll
+    for (int k = 0; k < kMapHalfPairs; ++k) {
+      const unsigned v = wA[base[k] + tw];
+      acc[k] = __hadd2_rn(acc[k], *reinterpret_cast<const __half2*>(&v));
+    }
+  }
+  __half* out = reinterpret_cast<__half*>(a.maps) + (size_t)vf * a.Hm * a.Wm;
+#pragma unroll
+  for (int k = 0; k < kMapHalfPairs; ++k) {
+    const int p = threadIdx.x + k * kMapHalfThreads;
+    if (p < npairs) {
+      const int row = p / npr, mx = 2 * (p - row * npr);
+      const size_t o = (size_t)(my0 + row) * a.Wm + mx;
+      out[o] = __low2half(acc[k]);
+      if (mx + 1 < a.Wm) out[o + 1] = __high2half(acc[k]);
+    }
+  }
+}
+
 // ------------------------------------------------------------------------
 // systematic points (per-mode formula; identical in the table kernel)
 // ------------------------------------------------------------------------

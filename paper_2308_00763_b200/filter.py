@@ -468,6 +468,16 @@ class Filter:
         est = self.run_frames(frame, 1)[:, 0, :]
         return (float(est[0, 0]), float(est[0, 1])) if self.n_tracks == 1 else est
 
+    def likelihood_maps(self, frames) -> np.ndarray:
+        """[F, H+2r, W+2r] per-position likelihood maps of host frames (mode dtype)."""
+        arr = np.ascontiguousarray(np.asarray(frames, dtype=np.uint8))
+        if arr.ndim == 2:
+            arr = arr[None]
+        r = int(np.max(np.abs(self._offs))) if self._offs.size else 0
+        out = np.empty((arr.shape[0], self.height + 2 * r, self.width + 2 * r), dtype=_DTYPE[self.mode])
+        N.check(N.lib().pf_likelihood_maps(self._h, N.ptr(arr), int(arr.shape[0]), N.ptr(out)), self._err)
+        return out
+
     def timings(self) -> Dict[str, float]:
         t = (C.c_float * 6)()
         N.check(N.lib().pf_last_timings(self._h, t), self._err)

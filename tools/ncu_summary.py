@@ -29,7 +29,7 @@ def raw(rep):
     rows = list(csv.reader(io.StringIO(out)))
     if len(rows) < 3:
         return {}
-    return dict(zip(rows[0], rows[2]))
+    return {k: (v, u) for k, u, v in zip(rows[0], rows[1], rows[2])}
 
 
 def main(rep, title):
@@ -42,9 +42,9 @@ def main(rep, title):
             print(f"| {k} | {got[k][0]} {got[k][1]} |")
     for k in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
         if k in d:
-            print(f"| {k} | {d[k]} |")
+            print(f"| {k} | {d[k][0]} {d[k][1]} |")
     stalls = []
-    for k, v in d.items():
+    for k, (v, _) in d.items():
         if k.startswith("smsp__average_warps_issue_stalled_") and k.endswith("_per_issue_active.ratio"):
             try:
                 stalls.append((float(v), k[len("smsp__average_warps_issue_stalled_"):-len("_per_issue_active.ratio")]))
