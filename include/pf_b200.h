@@ -37,6 +37,7 @@ extern "C" {
 #define PF_EDEGENERATE 2     /* DegeneracyError; frame index via pf_degenerate_frame */
 #define PF_ECUDA 3           /* CUDA runtime failure (message in pf_last_error) */
 #define PF_ENOMEM 4
+#define PF_EIO 5             /* I/O or container parse failure (cli.py exit code 3) */
 
 /* precisions (PrecisionMode, filter.py:49-60) */
 #define PF_FP64 0
@@ -106,6 +107,29 @@ int pf_last_timings(const pf_handle* h, float* ms6);
  * summed durations of the fused frame kernels / tile-table kernels alone
  * (events between launches on the handle's stream). */
 int pf_set_profiling(pf_handle* h, int32_t on);
+
+/* ---------------------------------------------------------------------------
+ * Input side of the step.
+ *
+ * pf_generate_video renders the reference's synthetic video model
+ * (model.generate_video, model.py:123-157) on the device: frames_dev receives
+ * [F][H][W] uint8, truth_host [F][2] (x, y) is the reference trajectory
+ * (specular bounces, model.py:105-121).  Pixel noise comes from the
+ * counter-based LCG ziggurat stream of `seed` (pixel (t, y, x) at stream
+ * position (t*H + y)*W + x), so frames are a pure function of (seed, t, y, x);
+ * oracle/video.py restates it.  Same model, not NumPy's PCG64 bytes.
+ *
+ * pf_pfvd_info / pf_read_pfvd ingest a PFVD container (model.py:274-297:
+ * "PFVD", u32 frames, width, height, pixels) straight into device memory
+ * through pinned double-buffered staging; fwh = {frames, width, height}.
+ * Errors: PF_EIO with the reference's messages ("bad container magic at
+ * offset 0", "truncated header at offset 4", "expected N pixel bytes at
+ * offset 16, got M"), readable with pf_global_error(). */
+int pf_generate_video(const pf_params* params, int32_t n_frames, int32_t width, int32_t height, double start_x,
+                      double start_y, uint64_t seed, const int32_t* offsets_xy, int32_t n_offsets,
+                      uint8_t* frames_dev, double* truth_host, int32_t device);
+int pf_pfvd_info(const char* path, int32_t* fwh);
+int pf_read_pfvd(const char* path, uint8_t* frames_dev, int64_t capacity, int32_t* fwh, int32_t device);
 
 /* ---------------------------------------------------------------------------
  * Sharded filter (one track, particle range split over n_shards <= 8 GPUs or

@@ -11,7 +11,9 @@ from .model import (
     Video,
     disk_template,
     generate_video,
+    generate_video_device,
     read_truth_csv,
+    read_video_device,
     read_video,
     write_truth_csv,
     write_video,
@@ -35,7 +37,8 @@ from .filter import (
 )
 
 __all__ = [
-    "ModelParams", "PixelTemplate", "Video", "disk_template", "generate_video",
+    "ModelParams", "PixelTemplate", "Video", "disk_template", "generate_video", "generate_video_device",
+    "read_video_device",
     "read_video", "write_video", "read_truth_csv", "write_truth_csv",
     "MAX_PARTICLES", "STAGES", "DegeneracyError", "Filter", "OpCounters", "ParticleSet",
     "PhiloxRngStream", "PrecisionMode", "RngStream", "RunResult", "accuracy_metrics", "init_particles",

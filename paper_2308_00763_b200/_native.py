@@ -14,7 +14,7 @@ import numpy as np
 LIB_PATH = os.environ.get("PF_B200_LIB") or os.path.join(os.path.dirname(os.path.abspath(__file__)), "lib",
                                                          "libpf_b200.so")
 
-PF_OK, PF_EINVAL, PF_EDEGENERATE, PF_ECUDA, PF_ENOMEM = 0, 1, 2, 3, 4
+PF_OK, PF_EINVAL, PF_EDEGENERATE, PF_ECUDA, PF_ENOMEM, PF_EIO = 0, 1, 2, 3, 4, 5
 PF_FP64, PF_FP32, PF_FP16, PF_FP16_PACKED = 0, 1, 2, 3
 
 
@@ -68,6 +68,10 @@ SIGNATURES = [
     ("pf_last_timings", C.c_int, [_VP, C.POINTER(C.c_float)]),
     ("pf_last_launches", C.c_int64, [_VP]),
     ("pf_set_trace", C.c_int, [_VP, C.c_int32]),
+    ("pf_generate_video", C.c_int, [C.POINTER(pf_params), C.c_int32, C.c_int32, C.c_int32, C.c_double, C.c_double,
+                                    C.c_uint64, _VP, C.c_int32, _VP, _VP, C.c_int32]),
+    ("pf_pfvd_info", C.c_int, [C.c_char_p, _VP]),
+    ("pf_read_pfvd", C.c_int, [C.c_char_p, _VP, C.c_int64, _VP, C.c_int32]),
     ("pf_shard_create", C.c_int, [C.POINTER(_VP), C.POINTER(pf_config), C.c_int32, C.c_int32]),
     ("pf_shard_info", C.c_int, [_VP, _VP]),
     ("pf_shard_buffers", C.c_int, [_VP, _VP]),

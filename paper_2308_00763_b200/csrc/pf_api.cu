@@ -12,12 +12,14 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <cstdio>
 #include <string>
 #include <vector>
 
 #include "../../include/pf_b200.h"
 #include "pf_kernels.cuh"
 #include "pf_staged.cuh"
+#include "pf_video.cuh"
 // host copies of the ziggurat tables
 #undef PF_ZIG_QUAL
 #define PF_ZIG_QUAL static const
@@ -971,6 +973,168 @@ int pf_get_debug(pf_handle* h, int32_t track, int64_t* anc, void* loglik) {
   if (anc) PF_CUDA(cudaMemcpy(anc, h->dbg_anc + track * K, K * 8, cudaMemcpyDeviceToHost), h->err);
   if (loglik)
     PF_CUDA(cudaMemcpy(loglik, (char*)h->dbg_L + track * K * h->rs, K * h->rs, cudaMemcpyDeviceToHost), h->err);
+  return PF_OK;
+}
+
+// ---------------------------------------------------------------------------
+// input side: device video rendering, PFVD ingest
+// ---------------------------------------------------------------------------
+// model._reflect (model.py:105-121): one step with specular bounces
+static void reflect_step(double& v, double& d, double hi) {
+  v += d;
+  while (v < 0.0 || v > hi) {
+    if (v < 0.0) {
+      v = -v;
+      d = -d;
+    }
+    if (v > hi) {
+      v = 2.0 * hi - v;
+      d = -d;
+    }
+  }
+}
+
+int pf_generate_video(const pf_params* params, int32_t F, int32_t W, int32_t H, double x0, double y0,
+                      uint64_t seed, const int32_t* offsets_xy, int32_t n_off, uint8_t* frames_dev,
+                      double* truth_host, int32_t device) {
+  if (!params || F < 1 || W < 1 || H < 1 || n_off < 1 || !offsets_xy || !frames_dev || !truth_host) {
+    g_err = "bad video arguments";
+    return PF_EINVAL;
+  }
+  if (F < 1) {
+    g_err = "frames must be at least 1";
+    return PF_EINVAL;
+  }
+  if (!(x0 >= 0.0 && x0 <= W - 1 && y0 >= 0.0 && y0 <= H - 1)) {
+    g_err = "start outside frame bounds";
+    return PF_EINVAL;
+  }
+  PF_CUDA(cudaSetDevice(device), g_err);
+  int rc = init_device_tables(device, g_err);
+  if (rc) return rc;
+  // truth trajectory and the clipped disk pixels per frame (model.py:136-155)
+  std::vector<int> fg((size_t)F * n_off);
+  double x = x0, y = y0, dx = params->drift_x, dy = params->drift_y;
+  for (int t = 0; t < F; ++t) {
+    truth_host[2 * t] = x;
+    truth_host[2 * t + 1] = y;
+    const long cx = (long)std::nearbyint(x), cy = (long)std::nearbyint(y);  // round half to even
+    for (int j = 0; j < n_off; ++j) {
+      const long col = std::min(std::max(offsets_xy[2 * j] + cx, 0L), (long)W - 1);
+      const long row = std::min(std::max(offsets_xy[2 * j + 1] + cy, 0L), (long)H - 1);
+      fg[(size_t)t * n_off + j] = (int)(row * W + col);
+    }
+    reflect_step(x, dx, W - 1.0);
+    reflect_step(y, dy, H - 1.0);
+  }
+  int* d_fg = nullptr;
+  PF_CUDA(cudaMalloc(&d_fg, fg.size() * sizeof(int)), g_err);
+  cudaError_t ce = cudaMemcpy(d_fg, fg.data(), fg.size() * sizeof(int), cudaMemcpyHostToDevice);
+  const long long frame_px = (long long)W * H, n = frame_px * F;
+  const unsigned long long xs = pfv::video_stream_state(seed);
+  if (ce == cudaSuccess) {
+    const long long threads = (n + 7) / 8;
+    pfv::render_background<<<(unsigned)((threads + 255) / 256), 256>>>(frames_dev, n, xs, params->bg_mean,
+                                                                         params->noise_std);
+    pfv::render_object<<<F, 128>>>(frames_dev, d_fg, n_off, frame_px, xs, params->fg_mean, params->noise_std);
+    ce = cudaDeviceSynchronize();
+  }
+  cudaFree(d_fg);
+  PF_CUDA(ce, g_err);
+  return PF_OK;
+}
+
+// PFVD container: "PFVD", u32 frames, width, height, pixels (model.py:274-297)
+int pf_pfvd_info(const char* path, int32_t* fwh) {
+  if (!path || !fwh) return PF_EINVAL;
+  FILE* fh = std::fopen(path, "rb");
+  if (!fh) {
+    g_err = std::string(path) + ": cannot open";
+    return PF_EIO;
+  }
+  char magic[4];
+  uint32_t hdr[3];
+  const size_t m = std::fread(magic, 1, 4, fh);
+  if (m != 4 || std::memcmp(magic, "PFVD", 4) != 0) {
+    std::fclose(fh);
+    g_err = std::string(path) + ": bad container magic at offset 0";
+    return PF_EIO;
+  }
+  if (std::fread(hdr, 4, 3, fh) != 3) {
+    std::fclose(fh);
+    g_err = std::string(path) + ": truncated header at offset 4";
+    return PF_EIO;
+  }
+  std::fseek(fh, 0, SEEK_END);
+  const long long payload = (long long)std::ftell(fh) - 16;
+  std::fclose(fh);
+  const long long expected = (long long)hdr[0] * hdr[1] * hdr[2];
+  if (payload != expected) {
+    g_err = std::string(path) + ": expected " + std::to_string(expected) + " pixel bytes at offset 16, got " +
+            std::to_string(payload);
+    return PF_EIO;
+  }
+  fwh[0] = (int32_t)hdr[0];
+  fwh[1] = (int32_t)hdr[1];
+  fwh[2] = (int32_t)hdr[2];
+  return PF_OK;
+}
+
+// streams the payload through two pinned staging buffers into device memory
+// (the read of chunk i+1 overlaps the copy of chunk i)
+int pf_read_pfvd(const char* path, uint8_t* frames_dev, int64_t capacity, int32_t* fwh, int32_t device) {
+  if (!frames_dev || !fwh) return PF_EINVAL;
+  int rc = pf_pfvd_info(path, fwh);
+  if (rc) return rc;
+  const long long total = (long long)fwh[0] * fwh[1] * fwh[2];
+  if (total > capacity) {
+    g_err = "device buffer too small for the video";
+    return PF_EINVAL;
+  }
+  PF_CUDA(cudaSetDevice(device), g_err);
+  FILE* fh = std::fopen(path, "rb");
+  if (!fh) {
+    g_err = std::string(path) + ": cannot open";
+    return PF_EIO;
+  }
+  std::fseek(fh, 16, SEEK_SET);
+  const size_t chunk = 8u << 20;
+  uint8_t* pin[2] = {nullptr, nullptr};
+  cudaEvent_t done[2] = {nullptr, nullptr};
+  cudaStream_t st = nullptr;
+  cudaError_t ce = cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking);
+  for (int i = 0; i < 2 && ce == cudaSuccess; ++i) {
+    ce = cudaMallocHost(&pin[i], chunk);
+    if (ce == cudaSuccess) ce = cudaEventCreateWithFlags(&done[i], cudaEventDisableTiming);
+  }
+  long long off = 0;
+  int k = 0;
+  while (ce == cudaSuccess && off < total) {
+    const size_t n = (size_t)std::min<long long>(chunk, total - off);
+    ce = cudaEventSynchronize(done[k]);  // the previous copy out of this staging buffer is done
+    if (ce != cudaSuccess) break;
+    if (std::fread(pin[k], 1, n, fh) != n) {
+      g_err = std::string(path) + ": short read";
+      ce = cudaErrorUnknown;
+      break;
+    }
+    ce = cudaMemcpyAsync(frames_dev + off, pin[k], n, cudaMemcpyHostToDevice, st);
+    if (ce == cudaSuccess) ce = cudaEventRecord(done[k], st);
+    off += (long long)n;
+    k ^= 1;
+  }
+  if (ce == cudaSuccess) ce = cudaStreamSynchronize(st);
+  std::fclose(fh);
+  for (int i = 0; i < 2; ++i) {
+    if (pin[i]) cudaFreeHost(pin[i]);
+    if (done[i]) cudaEventDestroy(done[i]);
+  }
+  if (st) cudaStreamDestroy(st);
+  if (ce != cudaSuccess) {
+    if (g_err.empty() || g_err.find("short read") == std::string::npos)
+      g_err = std::string("CUDA error ") + cudaGetErrorString(ce) + " reading PFVD";
+    return g_err.find("short read") != std::string::npos ? PF_EIO : PF_ECUDA;
+  }
   return PF_OK;
 }
 

@@ -165,3 +165,67 @@ def read_truth_csv(path) -> np.ndarray:
             raise ValueError(f"{path}: unexpected truth CSV header {head!r}")
         rows = [tuple(float(v) for v in line.strip().split(",")[1:]) for line in fh if line.strip()]
     return np.array(rows, dtype=np.float64).reshape(-1, 2)
+
+
+# --- device-side input ----------------------------------------
+
+
+def _lib():
+    from . import _native
+
+    return _native
+
+
+def generate_video_device(params: ModelParams, frames: int, width: int, height: int,
+                          start: Tuple[float, float], seed: int, device: int = 0):
+    """The reference video model rendered on the device (pf_generate_video).
+
+    Returns (frames: torch uint8 CUDA tensor [F, H, W], truth: (F, 2) float64).
+    Same model and trajectory as generate_video; the pixel noise comes from the
+    counter-based LCG stream of `seed` instead of NumPy's PCG64 (frames are a
+    pure function of (seed, t, y, x); oracle/video.py restates them)."""
+    import ctypes as C
+
+    import torch
+
+    N = _lib()
+    if frames < 1:
+        raise ValueError("frames must be at least 1")
+    x, y = float(start[0]), float(start[1])
+    if not (0.0 <= x <= width - 1 and 0.0 <= y <= height - 1):
+        raise ValueError(f"start {start} outside frame bounds {width}x{height}")
+    out = torch.empty((frames, height, width), dtype=torch.uint8, device=torch.device("cuda", device))
+    truth = np.empty((frames, 2), dtype=np.float64)
+    offs = np.ascontiguousarray(disk_template(params.disk_radius).offsets.astype(np.int32))
+    p = N.pf_params(params.drift_x, params.std_x, params.drift_y, params.std_y, params.bg_mean, params.fg_mean,
+                    params.likelihood_scale, params.disk_radius, params.noise_std)
+    rc = N.lib().pf_generate_video(C.byref(p), int(frames), int(width), int(height), x, y,
+                                   int(seed) & ((1 << 64) - 1), N.ptr(offs), int(offs.shape[0]),
+                                   C.c_void_p(out.data_ptr()), N.ptr(truth), int(device))
+    N.check(rc, N.lib().pf_global_error)
+    return out, truth
+
+
+def read_video_device(path, device: int = 0):
+    """PFVD container -> torch uint8 CUDA tensor [F, H, W] (pinned, double-buffered ingest)."""
+    import ctypes as C
+
+    import torch
+
+    N = _lib()
+    fwh = np.zeros(3, dtype=np.int32)
+    bpath = str(path).encode()
+    rc = N.lib().pf_pfvd_info(bpath, N.ptr(fwh))
+    if rc == N.PF_EIO:
+        msg = N.lib().pf_global_error().decode()
+        if msg.endswith("cannot open"):
+            raise FileNotFoundError(msg)
+        raise ValueError(msg)
+    N.check(rc, N.lib().pf_global_error)
+    F, W, H = (int(v) for v in fwh)
+    out = torch.empty((F, H, W), dtype=torch.uint8, device=torch.device("cuda", device))
+    rc = N.lib().pf_read_pfvd(bpath, C.c_void_p(out.data_ptr()), out.numel(), N.ptr(fwh), int(device))
+    if rc == N.PF_EIO:
+        raise ValueError(N.lib().pf_global_error().decode())
+    N.check(rc, N.lib().pf_global_error)
+    return out
