@@ -42,13 +42,14 @@ DTYPE_TAG = {"fp64": "f64", "fp32": "f32", "fp16": "f16", "fp16-packed": "f16"}
 CONFIGS = {
     "c1": dict(W=128, H=128, F=10, K=10_000, precision="fp64", tracks=1, videos=1,
                desc="C1: 128x128 video, 10 frames, 10,000 particles, FP64"),
-    "c2": dict(W=128, H=128, F=100, K=1_000_000, precision="fp16", tracks=1, videos=1,
-               desc="C2: 128x128 video, 100 frames, 1M particles, stabilised FP16 (FP32/FP64 alongside)"),
-    "c3": dict(W=1024, H=1024, F=100, K=1 << 24, precision="fp16", tracks=1, videos=1,
+    "c2": dict(W=128, H=128, F=100, K=1_000_000, precision="fp16-packed", tracks=1, videos=1,
+               desc="C2: 128x128 video, 100 frames, 1M particles, stabilised FP16 in half2 lanes "
+                    "(scalar-lane FP16, FP32, FP64 alongside)"),
+    "c3": dict(W=1024, H=1024, F=100, K=1 << 24, precision="fp16-packed", tracks=1, videos=1,
                desc="C3: 1024x1024 video, 100 frames, 16M particles, FP16 half2"),
-    "c4": dict(W=128, H=128, F=100, K=65536, precision="fp16", tracks=8192, videos=8,
+    "c4": dict(W=128, H=128, F=100, K=65536, precision="fp16-packed", tracks=8192, videos=8,
                desc="C4: 8192 independent 128x128 tracks x 64K particles, FP16 (tracks split over GPUs)"),
-    "c5": dict(W=1024, H=1024, F=10, K=1 << 30, precision="fp16", tracks=1, videos=1, sharded=True,
+    "c5": dict(W=1024, H=1024, F=10, K=1 << 30, precision="fp16-packed", tracks=1, videos=1, sharded=True,
                desc="C5: one 2^30-particle FP16 filter, 1024x1024 video, 10 frames, particle range sharded "
                     "over the GPUs (NCCL all-gathers of shard max / sums, peer reads of remote ancestors)"),
 }
@@ -442,7 +443,8 @@ def main():
     traffic = None
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as fh:
-            tr = json.load(fh).get(f"{args.config}_{prec}")
+            d = json.load(fh)
+            tr = d.get(f"{args.config}_{prec}") or d.get(f"{args.config}_{prec.split('-')[0]}")
             if tr:
                 traffic = tr["dram_bytes_per_launch"]
     except Exception:
@@ -457,7 +459,7 @@ def main():
     # ---- the other precisions of the same workload -----------------------
     extra = {}
     if not args.no_extra and args.config == "c2":
-        for p2 in ("fp32", "fp64"):
+        for p2 in ("fp16", "fp32", "fp64"):
             g = make(p2)
             device_steps(g, 2)
             ms2, _ = device_steps(g, max(3, args.steps // 2))
@@ -471,6 +473,7 @@ def main():
         extra[prec] = {"value": value, "unit": UNIT, "tracking_rmse_px": rmse, "tracking_mean_err_px": mean_err}
         extra["fp16_over_fp32"] = value / extra["fp32"]["value"]
         extra["fp16_over_fp64"] = value / extra["fp64"]["value"]
+        extra["packed_over_scalar_fp16"] = value / extra["fp16"]["value"]
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

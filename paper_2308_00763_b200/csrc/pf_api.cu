@@ -215,15 +215,15 @@ struct pf_handle {
 
 typedef void (*fused_fn)(pfk::FusedArgs);
 // (VPT, rounds) per threads-per-block: the tile is always PF_TILE particles
-template <int M>
+template <int M, bool PK = true>
 static fused_fn fused_for_tpb(int tpb) {
   switch (tpb) {
-    case 32: return pfk::pf_fused_frame<M, 8, 4>;
-    case 64: return pfk::pf_fused_frame<M, 8, 2>;
-    case 128: return pfk::pf_fused_frame<M, 8, 1>;
-    case 512: return pfk::pf_fused_frame<M, 2, 1>;
-    case 1024: return pfk::pf_fused_frame<M, 1, 1>;
-    default: return pfk::pf_fused_frame<M, 4, 1>;
+    case 32: return pfk::pf_fused_frame<M, 8, 4, false, PK>;
+    case 64: return pfk::pf_fused_frame<M, 8, 2, false, PK>;
+    case 128: return pfk::pf_fused_frame<M, 8, 1, false, PK>;
+    case 512: return pfk::pf_fused_frame<M, 2, 1, false, PK>;
+    case 1024: return pfk::pf_fused_frame<M, 1, 1, false, PK>;
+    default: return pfk::pf_fused_frame<M, 4, 1, false, PK>;
   }
 }
 // sharded filters: 128 or 256 threads per block only (keeps the instantiations few)
@@ -234,6 +234,7 @@ static fused_fn fused_sharded(int tpb) {
 static fused_fn fused_kernel(const pf_handle* h) {
   if (h->n_shards > 1)
     return h->km == 0 ? fused_sharded<0>(h->tpb) : h->km == 1 ? fused_sharded<1>(h->tpb) : fused_sharded<2>(h->tpb);
+  if (h->km == 2 && h->precision == PF_FP16) return fused_for_tpb<2, false>(h->tpb);  // scalar lanes
   return h->km == 0 ? fused_for_tpb<0>(h->tpb) : h->km == 1 ? fused_for_tpb<1>(h->tpb) : fused_for_tpb<2>(h->tpb);
 }
 static cudaError_t set_fused_smem(const pf_handle* h) {
@@ -539,7 +540,11 @@ static int create_impl(pf_handle** out, const pf_config* cfg, int n_shards, int 
     const pfk::MapHalfGeom g = pfk::map_half_geom(h->W, h->H, h->r, h->n_off);
     if (g.smem <= 200 * 1024) {
       h->map_img = true;
-      CK(cudack(cudaFuncSetAttribute(pfk::pf_map_half_img, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)g.smem),
+      CK(cudack(cudaFuncSetAttribute(pfk::pf_map_half_img<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)g.smem),
+                "map smem attr"));
+      CK(cudack(cudaFuncSetAttribute(pfk::pf_map_half_img<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)g.smem),
                 "map smem attr"));
     }
   }
@@ -650,7 +655,10 @@ static int launch_maps(pf_handle* h, const uint8_t* dframes, int F) {
   else if (h->map_img) {
     const pfk::MapHalfGeom g = pfk::map_half_geom(h->W, h->H, h->r, h->n_off);
     dim3 gi((h->Hm + g.band - 1) / g.band, h->n_videos * F);
-    pfk::pf_map_half_img<<<gi, pfk::kMapHalfThreads, g.smem, h->stream>>>(a);
+    if (h->precision == PF_FP16)  // scalar lanes ("fp16")
+      pfk::pf_map_half_img<false><<<gi, pfk::kMapHalfThreads, g.smem, h->stream>>>(a);
+    else
+      pfk::pf_map_half_img<true><<<gi, pfk::kMapHalfThreads, g.smem, h->stream>>>(a);
   } else
     pfk::pf_map_half<<<grid, 256, h->map_smem, h->stream>>>(a);
   h->launches += 1;

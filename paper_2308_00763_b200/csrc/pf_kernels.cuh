@@ -63,6 +63,17 @@ __device__ __forceinline__ double to_d(double v) { return v; }
 __device__ __forceinline__ double to_d(float v) { return (double)v; }
 __device__ __forceinline__ double to_d(__half v) { return (double)__half2float(v); }
 
+// "naive" binary16 ops of the scalar-lane kernels: half storage, f32 compute,
+// every result rounded back to binary16 -- RN16(RN32(a op b)) == RN16(a op b)
+// for + and * (24 >= 2*11 + 2 bits: double rounding is innocuous), so values
+// equal the native half2 path.  (Scalar add.rn.f16 was tried first: ptxas
+// re-pairs adjacent lanes into one HADD2 -- measured in the SASS.)
+__device__ __forceinline__ __half hadd_s(__half a, __half b) {
+  return __float2half_rn(__fadd_rn(__half2float(a), __half2float(b)));
+}
+__device__ __forceinline__ __half hmul_s(__half a, __half b) {
+  return __float2half_rn(__fmul_rn(__half2float(a), __half2float(b)));
+}
 // ------------------------------------------------------------------------
 // TMA bulk copy helpers (cp.async.bulk + mbarrier)
 // ------------------------------------------------------------------------
@@ -290,6 +301,7 @@ __host__ __device__ inline MapHalfGeom map_half_geom(int W, int H, int r, int n_
   return g;
 }
 
+template <bool PK>  // PK: one HADD2 per entry pair and tap; else two scalar HADDs (same values)
 __global__ void __launch_bounds__(kMapHalfThreads) pf_map_half_img(MapArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
   const MapHalfGeom g = map_half_geom(a.W, a.H, a.r, a.n_off);
@@ -361,7 +373,12 @@ __global__ void __launch_bounds__(kMapHalfThreads) pf_map_half_img(MapArgs a) {
 #pragma unroll
     for (int k = 0; k < kMapHalfPairs; ++k) {
       const unsigned v = wA[base[k] + tw];
-      acc[k] = __hadd2_rn(acc[k], *reinterpret_cast<const __half2*>(&v));
+      const __half2 tv = *reinterpret_cast<const __half2*>(&v);
+      if constexpr (PK)
+        acc[k] = __hadd2_rn(acc[k], tv);
+      else
+        acc[k] = __halves2half2(hadd_s(__low2half(acc[k]), __low2half(tv)), hadd_s(__high2half(acc[k]), __high2half(tv)));
+
     }
   }
   __half* out = reinterpret_cast<__half*>(a.maps) + (size_t)vf * a.Hm * a.Wm;
@@ -718,6 +735,18 @@ __device__ __forceinline__ typename Tr<MODE>::vec to_vec(double n0, double n1) {
   return v;
 }
 
+// "fp16" (scalar lanes, the reference's FP16_SCALAR engine): the same RN16
+// ops one lane at a time -- the naive half of the paper's naive-vs-packed
+// kernel pair; values are identical to the half2 path (hadd_s / hmul_s)
+__device__ __forceinline__ __half2 scale_noise_scalar(__half2 nn, __half2 stdv) {
+  return __halves2half2(hmul_s(__low2half(stdv), __low2half(nn)), hmul_s(__high2half(stdv), __high2half(nn)));
+}
+__device__ __forceinline__ __half2 prop_scalar(__half2 xa, __half2 sn, __half2 drift) {
+  const __half x = hadd_s(hadd_s(__low2half(xa), __low2half(drift)), __low2half(sn));
+  const __half y = hadd_s(hadd_s(__high2half(xa), __high2half(drift)), __high2half(sn));
+  return __halves2half2(x, y);
+}
+
 // propagate with the scaled noise sn = d(std) * d(n) already formed:
 // x' = (x[a] + d(drift)) + sn, each op rounded separately (reference arithmetic)
 template <int MODE>
@@ -842,7 +871,9 @@ __device__ __forceinline__ double tree_vpt(const double* v) {
 
 // One CTA = one tile of PF_TILE particles of one track; TPB = PF_TILE/(VPT*R)
 // threads, thread t of round r owns particles (r*TPB + t)*VPT .. +VPT-1.
-template <int MODE, int VPT, int R, bool SH = false>  // SH: sharded filter (source tiles on several shards)
+// SH: sharded filter (source tiles on several shards); PK: FP16 in packed
+// half2 lanes (false: scalar lanes, "fp16" mode -- same values)
+template <int MODE, int VPT, int R, bool SH = false, bool PK = true>
 __global__ void __launch_bounds__(PF_TILE / (VPT * R)) pf_fused_frame(FusedArgs a) {
   using real = typename Tr<MODE>::real;
   using vec = typename Tr<MODE>::vec;
@@ -976,7 +1007,10 @@ __global__ void __launch_bounds__(PF_TILE / (VPT * R)) pf_fused_frame(FusedArgs 
         // fast-path test rabs < ki on the top 32 bits of rabs (bits 23..54 of w)
         slow |= (__funnelshift_r(wlo, whi, 23) >= s_kihi[idx] ? 1u : 0u) << (2 * i + c);
       }
-      s_X[l0 + i] = scale_noise<MODE>(to_vec<MODE>(nn[0], nn[1]), stdv);
+      if constexpr (MODE == M_FP16 && !PK)
+        s_X[l0 + i] = scale_noise_scalar(to_vec<MODE>(nn[0], nn[1]), stdv);
+      else
+        s_X[l0 + i] = scale_noise<MODE>(to_vec<MODE>(nn[0], nn[1]), stdv);
     }
     if (l0 + VPT > Tb) slow = l0 >= Tb ? 0u : slow & ((1u << (2 * (Tb - l0))) - 1u);
     while (slow) {  // rare per thread: re-derive the word by stepping from xs0
@@ -1216,7 +1250,11 @@ __global__ void __launch_bounds__(PF_TILE / (VPT * R)) pf_fused_frame(FusedArgs 
 #pragma unroll
       for (int i = 0; i < VPT; ++i) {
         if (in_tile(i)) {
-          const vec xn = prop<MODE>(xa[i], s_X[l0 + i], drift);
+          vec xn;
+          if constexpr (MODE == M_FP16 && !PK)
+            xn = prop_scalar(xa[i], s_X[l0 + i], drift);
+          else
+            xn = prop<MODE>(xa[i], s_X[l0 + i], drift);
           const int ix = round_clamp<MODE>(xn.x, mlo, mhx);
           const int iy = round_clamp<MODE>(xn.y, mlo, mhy);
           Lr[rr][i] = __ldg(mapc + iy * Wm + ix);

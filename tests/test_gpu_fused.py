@@ -78,9 +78,11 @@ def test_fused_bitexact_vs_oracle_acceptance(pf, acceptance_video, mode):
     assert np.array_equal(c.view(np.uint8), tr.c.view(np.uint8))
 
 
-@pytest.mark.parametrize("mode", ["fp64", "fp32", "fp16"])
+@pytest.mark.parametrize("mode", ["fp64", "fp32", "fp16", "fp16-packed"])
 @pytest.mark.parametrize("K", [2, 1023, 1025, 10_000, 40_961, 200_003])
 def test_fused_bitexact_vs_oracle_sizes(pf, mode, K):
+    if mode == "fp16-packed" and K % 2:
+        pytest.skip("packed binary16 needs an even particle count (filter.py:137-143)")
     frames, _ = rp.generate_video(rp.Params(), 6, 96, 80, (40.0, 30.0), 17)
     traj = pf.Filter(K, mode, 96, 80, 5, start_hint=(40.0, 30.0)).run(frames)
     ref, _ = fused.run(frames, K, mode, 5, start_hint=(40.0, 30.0))
@@ -165,3 +167,16 @@ def test_run_api_fused(pf, acceptance_video):
     assert np.array_equal(res.trajectory, ref)
     assert set(res.stage_ms) == set(pf.STAGES)
     assert res.launches == 1 + 2 * 100
+
+
+@pytest.mark.parametrize("tpb", [32, 128, 256, 1024])
+def test_fp16_scalar_and_packed_kernels_identical(pf, tpb):
+    """The naive-vs-optimised pair: "fp16" runs the scalar-lane
+    kernels (one RN16 op per lane), "fp16-packed" the half2 kernels; values are
+    identical (reference test_acceptance.py:233-248), only the pipes differ."""
+    frames, _ = rp.generate_video(rp.Params(), 8, 128, 96, (64.0, 48.0), 21)
+    a = pf.Filter(50_000, "fp16", 128, 96, 3, tpb=tpb)
+    b = pf.Filter(50_000, "fp16-packed", 128, 96, 3, tpb=tpb)
+    assert np.array_equal(a.run(frames), b.run(frames))
+    assert np.array_equal(a.state()[2].view(np.uint16), b.state()[2].view(np.uint16))
+    assert np.array_equal(a.likelihood_maps(frames[:2]).view(np.uint16), b.likelihood_maps(frames[:2]).view(np.uint16))

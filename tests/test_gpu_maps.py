@@ -23,12 +23,12 @@ def _maps(mode, frames, template=None, params=None):
 
 
 def _oracle(mode, frame, offs, p):
-    if mode == "fp16":
+    if mode.startswith("fp16"):
         return rp.loglik_map_half(frame, offs, p)
     return rp.loglik_map_wide(frame, offs, p, np.float64 if mode == "fp64" else np.float32)
 
 
-@pytest.mark.parametrize("mode", ["fp16", "fp32", "fp64"])
+@pytest.mark.parametrize("mode", ["fp16", "fp16-packed", "fp32", "fp64"])
 @pytest.mark.parametrize("W,H", [(128, 128), (77, 53), (96, 80)])
 def test_maps_disk_template(mode, W, H):
     frames, _ = rp.generate_video(rp.Params(), 3, W, H, (W / 2.0, H / 2.0), 7)
@@ -36,14 +36,16 @@ def test_maps_disk_template(mode, W, H):
     offs = rp.disk_offsets(5)
     for t in range(3):
         ref = _oracle(mode, frames[t], offs, rp.Params())
-        assert np.array_equal(got[t].view(np.uint16 if mode == "fp16" else got.dtype).ravel(),
-                              ref.astype(got.dtype).view(np.uint16 if mode == "fp16" else got.dtype).ravel())
+        half = mode.startswith("fp16")
+        assert np.array_equal(got[t].view(np.uint16 if half else got.dtype).ravel(),
+                              ref.astype(got.dtype).view(np.uint16 if half else got.dtype).ravel())
 
 
-def test_maps_c3_frame_fp16():
+@pytest.mark.parametrize("mode", ["fp16", "fp16-packed"])
+def test_maps_c3_frame_fp16(mode):
     frames, _ = rp.generate_video(rp.Params(), 1, 1024, 1024, (512.0, 512.0), 42)
-    got = _maps("fp16", frames)[0]
-    ref = _oracle("fp16", frames[0], rp.disk_offsets(5), rp.Params())
+    got = _maps(mode, frames)[0]
+    ref = _oracle(mode, frames[0], rp.disk_offsets(5), rp.Params())
     assert np.array_equal(got.view(np.uint16), ref.view(np.uint16))
 
 
