@@ -567,7 +567,9 @@ static int create_impl(pf_handle** out, const pf_config* cfg, int n_shards, int 
     CK(cudack(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, tk, h->tpb_table, 0), "occupancy"));
     CK(cudack(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, h->device), "attr"));
     const char* force = std::getenv("PF_FORCE_SPLIT_TABLE");  // test knob: exercise the split path small
-    if ((long long)h->n_chunks * h->n_tracks > (long long)per_sm * sms / 2 ||
+    // (one track's chunks wait only for each other and are launched
+    // contiguously, so the bound is per track; single-chunk tables never spin)
+    if ((h->n_chunks > 1 && (long long)h->n_chunks > (long long)per_sm * sms / 2) ||
         (force && force[0] == '1' && h->n_tracks == 1)) {
       if (h->n_tracks != 1) {
         e = "too many table chunks for co-residency with several tracks (split the batch)";

@@ -180,3 +180,13 @@ def test_fp16_scalar_and_packed_kernels_identical(pf, tpb):
     assert np.array_equal(a.run(frames), b.run(frames))
     assert np.array_equal(a.state()[2].view(np.uint16), b.state()[2].view(np.uint16))
     assert np.array_equal(a.likelihood_maps(frames[:2]).view(np.uint16), b.likelihood_maps(frames[:2]).view(np.uint16))
+
+
+def test_c4_scale_batch_creates_and_steps(pf):
+    # 8192 tracks x 64K particles (C4 on one GPU): one table CTA per track, no
+    # cross-CTA co-residency requirement -- creation must not refuse it
+    frames, _ = rp.generate_video(rp.Params(), 2, 128, 128, (64.0, 64.0), 42)
+    f = pf.Filter(65536, "fp16-packed", 128, 128, seeds=list(range(8192)), n_tracks=8192)
+    traj = f.run(frames)
+    assert traj.shape == (8192, 2, 2) and np.isfinite(traj).all()
+    f.close()
