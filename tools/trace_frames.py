@@ -59,6 +59,8 @@ def main():
 
         def rel(a):
             a = a[a > 0]
+            if a.size == 0:
+                return (float("nan"), float("nan"))
             return (a.min() - t0) / 1e3, (a.max() - t0) / 1e3
 
         rows.append(dict(
@@ -70,6 +72,14 @@ def main():
     med = {k: (np.median([r[k][0] for r in rows[1:]]), np.median([r[k][1] for r in rows[1:]])) for k in keys}
     for k in keys:
         print(f"  {k:8s} first {med[k][0]:8.2f} us   last {med[k][1]:8.2f} us")
+    # mean per-CTA phase durations (frames 1..F-1)
+    fu = buf[1:, :nt].reshape(-1, 8).astype(np.float64)
+    ok = (fu[:, :6] > 0).all(axis=1)
+    fu = fu[ok]
+    names = ["draws", "wait", "window", "particles", "tail"]
+    d = np.diff(fu[:, :6], axis=1) / 1e3
+    print("  mean per-CTA phase (us): " + ", ".join(f"{n} {v:.2f}" for n, v in zip(names, d.mean(axis=0))) +
+          f"  | lifetime {(fu[:, 5] - fu[:, 0]).mean() / 1e3:.2f}")
     t0s = np.array([r["t0"] for r in rows])
     print(f"  period (fused entry to entry): median {np.median(np.diff(t0s))/1e3:.2f} us")
     rel0 = np.array([r["t0"] + r["release"][0] * 1e3 for r in rows])
