@@ -441,12 +441,14 @@ def main():
     peak, peak_src = _peaks()
     achieved = bytes_per_launch / (fused_avg_ms * 1e-3) / 1e9
     traffic = None
+    warp_inst = None
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as fh:
             d = json.load(fh)
             tr = d.get(f"{args.config}_{prec}") or d.get(f"{args.config}_{prec.split('-')[0]}")
             if tr:
                 traffic = tr["dram_bytes_per_launch"]
+                warp_inst = tr.get("warp_inst_per_launch")
     except Exception:
         pass
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
@@ -454,6 +456,18 @@ def main():
                 "algorithmic_bytes_per_launch": bytes_per_launch,
                 "bytes_per_particle": 6 * s, "avg_launch_ms": fused_avg_ms, "tile_table_avg_ms": table_avg_ms,
                 "maps_ms_per_step": tm["maps"], "peak_source": peak_src}
+    if warp_inst:
+        # the bound that binds: instruction issue, 4 warp-instructions
+        # per clock per SM; instruction count from the committed ncu capture
+        import torch
+
+        sms = torch.cuda.get_device_properties(local).multi_processor_count
+        mhz = (clk or {}).get("sm_mhz") or 1965
+        peak_issue = sms * 4 * mhz * 1e6
+        ach_issue = warp_inst / (fused_avg_ms * 1e-3)
+        roofline["issue"] = {"achieved": ach_issue, "peak": peak_issue, "unit": "warp-inst/s",
+                             "frac": ach_issue / peak_issue, "warp_inst_per_launch": warp_inst,
+                             "source": "ncu Executed Instructions (profiles/ncu_traffic.json), live launch time"}
     f.close()
 
     # ---- the other precisions of the same workload -----------------------

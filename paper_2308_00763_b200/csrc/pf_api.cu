@@ -426,6 +426,10 @@ static int create_impl(pf_handle** out, const pf_config* cfg, int n_shards, int 
   // tile table: one tile per thread; a single CTA up to 1024 tiles (the
   // cross-CTA exchanges cost more than they save there), chunks of 256 above
   h->tpb_table = h->n_pad <= 1024 ? std::max(32, h->n_pad) : 256;
+  if (const char* tt = std::getenv("PF_TABLE_TPB")) {  // A/B knob: tiles per table CTA
+    const int v = std::atoi(tt);
+    if (v >= 32 && v <= 1024 && (v & (v - 1)) == 0) h->tpb_table = std::min(h->tpb_table, v);
+  }
   h->n_chunks = (h->n_tiles + h->tpb_table - 1) / h->tpb_table;
   std::string& e = h->err;
 #define CK(x)                    \
