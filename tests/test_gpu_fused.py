@@ -190,3 +190,15 @@ def test_c4_scale_batch_creates_and_steps(pf):
     traj = f.run(frames)
     assert traj.shape == (8192, 2, 2) and np.isfinite(traj).all()
     f.close()
+
+
+@pytest.mark.parametrize("mode", ["fp16", "fp16-packed", "fp32"])
+def test_saturated_frame_stays_finite(pf, mode):
+    # reference test_model.py:169-190: on an all-255 frame the direct FP16
+    # likelihood overflows; the stabilised (log-domain, max-shifted) path stays
+    # finite and never degenerates
+    frames = np.full((5, 64, 64), 255, dtype=np.uint8)
+    traj = pf.Filter(20_000, mode, 64, 64, 3).run(frames)
+    assert np.isfinite(traj).all()
+    L = pf.Filter(64, mode, 64, 64, 3).likelihood_maps(frames[:1])
+    assert np.isfinite(np.asarray(L, dtype=np.float64)).all()
