@@ -994,8 +994,6 @@ __global__ void __launch_bounds__(PF_TILE / (VPT * R)) pf_fused_frame(FusedArgs 
         const unsigned long long w = xs;
         xs = pfr::kA * xs + pfr::kC;
         const unsigned whi = (unsigned)(w >> 32), wlo = (unsigned)w;
-        // layer (bits 56..63) and sign (bit 55) select a signed table entry:
-        // rabs * (-wi) == -(rabs * wi) exactly
         // rabs = bits 3..54 of w; (double)rabs exactly via the 2^52 bias trick
         const unsigned rlo = __funnelshift_r(wlo, whi, 3);
         const unsigned rhi = (whi >> 3) & 0xfffffu;
