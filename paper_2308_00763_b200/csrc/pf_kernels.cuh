@@ -1042,12 +1042,16 @@ __global__ void __launch_bounds__(PF_TILE / (VPT * R)) pf_fused_frame(FusedArgs 
         // relaxed polling (an acquire per poll would invalidate the SM's L1
         // under the CTAs still working on the previous frame), one acquire
         // fence once the counter is reached
-        for (;;) {
-          asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(rc) : "memory");
-          if (v >= a.ready_target) break;
-          __nanosleep(32);
+        // first look with acquire semantics: when the table is long done
+        // (every CTA after the first wave) no separate fence is needed
+        asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(rc) : "memory");
+        if (v < a.ready_target) {
+          do {
+            __nanosleep(32);
+            asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(rc) : "memory");
+          } while (v < a.ready_target);
+          asm volatile("fence.acq_rel.gpu;" ::: "memory");
         }
-        asm volatile("fence.acq_rel.gpu;" ::: "memory");
       }
       __syncwarp();
     } else {
