@@ -314,6 +314,8 @@ def main():
     ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
     ap.add_argument("--precision", default=None)
     ap.add_argument("--tpb", type=int, default=0, help="threads per block (0 = library default per precision)")
+    ap.add_argument("--tracks", type=int, default=0,
+                    help="override the config's track count (e.g. one rank's share of C4: 8192 / N)")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-extra", action="store_true", help="skip the FP32/FP64 side measurements")
@@ -322,6 +324,8 @@ def main():
     cfg = dict(CONFIGS[args.config])
     if args.precision:
         cfg["precision"] = args.precision
+    if args.tracks:
+        cfg["tracks"] = args.tracks
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
@@ -503,7 +507,10 @@ def main():
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": dev_ms / args.steps, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": DTYPE_TAG[prec], "data": "synthetic",
+            # a fixed batch of tracks split over the ranks is strong scaling; one
+            # independent track per rank (C2 at N GPUs) is weak scaling
+            "scaling": "strong" if cfg["tracks"] > 1 else "weak", "vs_baseline": None,
+            "dtype": DTYPE_TAG[prec], "data": "synthetic",
             "config": _config_block(cfg, args),
             "e2e": e2e, "roofline": roofline, "cpu_baseline": cpu, "clocks": clk,
             "gpu_launches": launches,
