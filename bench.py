@@ -314,6 +314,8 @@ def main():
     ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
     ap.add_argument("--precision", default=None)
     ap.add_argument("--tpb", type=int, default=0, help="threads per block (0 = library default per precision)")
+    ap.add_argument("--particles", type=int, default=0,
+                    help="override particles per track (e.g. one shard's share of C5: 2^30 / N)")
     ap.add_argument("--tracks", type=int, default=0,
                     help="override the config's track count (e.g. one rank's share of C4: 8192 / N)")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
@@ -326,6 +328,8 @@ def main():
         cfg["precision"] = args.precision
     if args.tracks:
         cfg["tracks"] = args.tracks
+    if args.particles:
+        cfg["K"] = args.particles
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
