@@ -238,7 +238,7 @@ def run_reference_arm(args, cfg, rank, world):
 def _config_block(cfg, args):
     return {"workload": cfg["desc"], "width": cfg["W"], "height": cfg["H"], "frames": cfg["F"],
             "particles_per_track": cfg["K"], "tracks": cfg["tracks"], "precision": cfg["precision"],
-            "tpb": args.tpb or "library default (fp16: 128 up to 2048 CTAs, else 256)", "l2": "flushed (512 MiB write) before every timed step",
+            "tpb": args.tpb or "library default (fp16/fp32: 128 up to 2048 CTAs, else 256; fp64: 256)", "l2": "flushed (512 MiB write) before every timed step",
             "rng": "counter-based LCG (device)", "parallelism": f"tracks/GPU, {args.gpus} GPU(s), no collective"}
 
 

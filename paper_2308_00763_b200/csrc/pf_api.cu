@@ -377,11 +377,12 @@ static int create_impl(pf_handle** out, const pf_config* cfg, int n_shards, int 
   h->H = cfg->height;
   h->n_tracks = cfg->n_tracks;
   h->n_videos = cfg->n_videos;
-  // default threads per block per precision (measured, bench TPB sweep)
-  // FP16 prefers 128 threads while the grid fits in about one wave, 256 beyond
+  // default threads per block per precision (measured, bench TPB sweeps):
+  // FP16 / FP32 prefer 128 threads while the grid fits in about one wave
+  // (C2: FP32 3.9e10 at 128 vs 3.3e10 at 256), 256 beyond; FP64 256
   {
     const long long ctas = ((cfg->K + PF_TILE - 1) / PF_TILE) * (long long)cfg->n_tracks;
-    h->tpb = cfg->tpb ? cfg->tpb : (cfg->precision >= PF_FP16 && ctas <= 2048 ? 128 : 256);
+    h->tpb = cfg->tpb ? cfg->tpb : (cfg->precision != PF_FP64 && ctas <= 2048 ? 128 : 256);
   }
   if (n_shards > 1 && h->tpb != 128) h->tpb = 256;  // sharded kernels exist for 128 / 256 threads
   h->vpt = h->tpb >= 1024 ? 1 : h->tpb >= 512 ? 2 : h->tpb >= 256 ? 4 : 8;
