@@ -175,6 +175,7 @@ struct pf_handle {
   double* d_traj = nullptr;
   size_t traj_cap = 0;
   int* d_degen = nullptr;
+  int* h_degen = nullptr;  // pinned host copy of d_degen
   long long* dbg_anc = nullptr;
   void* dbg_L = nullptr;
   long long frame_counter = 0;
@@ -316,6 +317,7 @@ int pf_destroy(pf_handle* h) {
       for (int i = 0; i < 8; ++i)
         if (h->peer[sh][i]) cudaIpcCloseMemHandle(h->peer[sh][i]);
   if (h->xev) cudaEventDestroy(h->xev);
+  if (h->h_degen) cudaFreeHost(h->h_degen);
   for (auto& e : h->ev)
     if (e) cudaEventDestroy(e);
   for (auto& e : h->pev) cudaEventDestroy(e);
@@ -787,11 +789,19 @@ static int launch_frame(pf_handle* h, const void* map_slot, long long map_video_
   return PF_OK;
 }
 
-static int finish_degenerate(pf_handle* h) {
-  std::vector<int> dg(h->n_tracks);
-  PF_CUDA(cudaMemcpy(dg.data(), h->d_degen, h->n_tracks * sizeof(int), cudaMemcpyDeviceToHost), h->err);
+// degeneracy flags: copied into pinned host memory on the stream (before the
+// run's synchronisation), so the check costs no extra blocking copy
+static int queue_degenerate(pf_handle* h) {
+  if (!h->h_degen) PF_CUDA(cudaMallocHost(&h->h_degen, (size_t)h->n_tracks * sizeof(int)), h->err);
+  PF_CUDA(cudaMemcpyAsync(h->h_degen, h->d_degen, (size_t)h->n_tracks * sizeof(int), cudaMemcpyDeviceToHost,
+                          h->stream),
+          h->err);
+  return PF_OK;
+}
+
+static int finish_degenerate(pf_handle* h) {  // after the stream is synchronised
   int m = INT_MAX;
-  for (int v : dg) m = std::min(m, v);
+  for (int i = 0; i < h->n_tracks; ++i) m = std::min(m, h->h_degen[i]);
   if (m != INT_MAX) {
     h->degenerate_frame = m;
     h->err = "weight sum degenerated (frame " + std::to_string(m) + ")";
@@ -878,6 +888,7 @@ int pf_run(pf_handle* h, const uint8_t* frames, int32_t F, int32_t on_device, do
   PF_CUDA(cudaEventRecord(h->ev[3], h->stream), h->err);
   PF_CUDA(cudaMemcpyAsync(traj_out, h->d_traj, (size_t)h->n_tracks * F * 2 * 8, cudaMemcpyDeviceToHost, h->stream),
           h->err);
+  if ((rc = queue_degenerate(h))) return rc;
   PF_CUDA(cudaEventRecord(h->ev[4], h->stream), h->err);
   PF_CUDA(cudaStreamSynchronize(h->stream), h->err);
   float ms;
@@ -1348,6 +1359,8 @@ int pf_shard_end(pf_handle* h, int32_t F, double* traj_out) {
   PF_CUDA(cudaSetDevice(h->device), h->err);
   PF_CUDA(cudaEventRecord(h->ev[3], h->stream), h->err);
   PF_CUDA(cudaMemcpyAsync(traj_out, h->d_traj, (size_t)F * 2 * 8, cudaMemcpyDeviceToHost, h->stream), h->err);
+  int rc = queue_degenerate(h);
+  if (rc) return rc;
   PF_CUDA(cudaEventRecord(h->ev[4], h->stream), h->err);
   PF_CUDA(cudaStreamSynchronize(h->stream), h->err);
   float ms = 0.f;
