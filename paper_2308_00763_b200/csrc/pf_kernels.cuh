@@ -869,12 +869,23 @@ __device__ __forceinline__ double tree_vpt(const double* v) {
     return v[0];
 }
 
+// Minimum resident CTAs per SM (register budget) of the 256-thread variants,
+// measured on C3 (same-box A/B): FP16 7 (32 registers, a few spills) 5.37 ->
+// 5.64e10, FP32 6 (40 registers) 4.30 -> 4.45e10; FP64 5 (48 registers; 40
+// lose 3%); the 128-thread variants keep the compiler's choice (C2 FP16 at 40
+// registers: -9%).
+template <int MODE>
+constexpr int fused_min_blocks(int tpb) {
+  return tpb != 256 ? 0 : MODE == M_FP16 ? 7 : MODE == M_FP32 ? 6 : 5;  // 0: no constraint
+}
+
 // One CTA = one tile of PF_TILE particles of one track; TPB = PF_TILE/(VPT*R)
 // threads, thread t of round r owns particles (r*TPB + t)*VPT .. +VPT-1.
 // SH: sharded filter (source tiles on several shards); PK: FP16 in packed
 // half2 lanes (false: scalar lanes, "fp16" mode -- same values)
 template <int MODE, int VPT, int R, bool SH = false, bool PK = true>
-__global__ void __launch_bounds__(PF_TILE / (VPT * R)) pf_fused_frame(FusedArgs a) {
+__global__ void __launch_bounds__(PF_TILE / (VPT * R), fused_min_blocks<MODE>(PF_TILE / (VPT * R)))
+    pf_fused_frame(FusedArgs a) {
   using real = typename Tr<MODE>::real;
   using vec = typename Tr<MODE>::vec;
   using wq_t = typename Tr<MODE>::wq_t;
