@@ -1035,6 +1035,10 @@ int pf_generate_video(const pf_params* params, int32_t F, int32_t W, int32_t H, 
     g_err = "start outside frame bounds";
     return PF_EINVAL;
   }
+  if ((W == 1 && params->drift_x != 0.0) || (H == 1 && params->drift_y != 0.0)) {
+    g_err = "a 1-pixel frame axis with non-zero drift has no bounded trajectory";
+    return PF_EINVAL;  // (the reference's bounce loop would never end)
+  }
   PF_CUDA(cudaSetDevice(device), g_err);
   int rc = init_device_tables(device, g_err);
   if (rc) return rc;

@@ -103,10 +103,18 @@ def _bounce(pos: float, step: float, hi: float) -> Tuple[float, float]:
     return pos, step
 
 
+def _check_bounce(params: ModelParams, width: int, height: int) -> None:
+    # the reference's bounce loop (model.py:105-121) never ends on a 1-pixel
+    # axis with a non-zero drift; refuse instead of hanging
+    if (width == 1 and params.drift_x != 0.0) or (height == 1 and params.drift_y != 0.0):
+        raise ValueError("a 1-pixel frame axis with non-zero drift has no bounded trajectory")
+
+
 def generate_video(params: ModelParams, frames: int, width: int, height: int,
                    start: Tuple[float, float], seed: int) -> Video:
     if frames < 1:
         raise ValueError("frames must be at least 1")
+    _check_bounce(params, width, height)
     x, y = float(start[0]), float(start[1])
     if not (0.0 <= x <= width - 1 and 0.0 <= y <= height - 1):
         raise ValueError(f"start {start} outside frame bounds {width}x{height}")
@@ -191,6 +199,7 @@ def generate_video_device(params: ModelParams, frames: int, width: int, height: 
     N = _lib()
     if frames < 1:
         raise ValueError("frames must be at least 1")
+    _check_bounce(params, width, height)
     x, y = float(start[0]), float(start[1])
     if not (0.0 <= x <= width - 1 and 0.0 <= y <= height - 1):
         raise ValueError(f"start {start} outside frame bounds {width}x{height}")
