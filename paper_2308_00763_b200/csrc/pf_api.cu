@@ -186,6 +186,9 @@ struct pf_handle {
   int degenerate_frame = -1;
   size_t map_smem = 0, fused_smem = 0;
   int map_band = 32;
+  bool map_wide_img = false;  // FP32 / FP64 term-image map kernel
+  int map_wide_band = 8;
+  size_t map_wide_smem = 0;
   bool map_img = false;  // binary16 term-image map kernel
   bool profiling = false;
   std::vector<cudaEvent_t> pev;  // 3 per frame when profiling
@@ -555,6 +558,22 @@ static int create_impl(pf_handle** out, const pf_config* cfg, int n_shards, int 
                 "map smem attr"));
     }
   }
+  // FP32 / FP64: the term-image kernel for single-leaf templates when a band fits
+  h->map_wide_img = false;
+  if (h->km != 2 && h->n_plan == 1) {
+    int band = h->W >= 512 ? 8 : 32;
+    while (band > 1 && pfk::map_wide_geom(h->W, h->r, h->n_off, h->rs, band).smem > 200 * 1024) band /= 2;
+    const pfk::MapWideGeom g = pfk::map_wide_geom(h->W, h->r, h->n_off, h->rs, band);
+    if (g.smem <= 200 * 1024 && std::getenv("PF_MAP_GENERIC") == nullptr) {
+      h->map_wide_img = true;
+      h->map_wide_band = band;
+      h->map_wide_smem = g.smem;
+      CK(cudack(cudaFuncSetAttribute(h->km == 0 ? (const void*)pfk::pf_map_wide_img<double>
+                                                : (const void*)pfk::pf_map_wide_img<float>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)g.smem),
+                "map smem attr"));
+    }
+  }
   if (h->map_smem > 48 * 1024) {
     cudaError_t ce = cudaSuccess;
     if (h->km == 0)
@@ -657,7 +676,17 @@ static int launch_maps(pf_handle* h, const uint8_t* dframes, int F) {
   a.maps = h->d_maps;
   a.band = h->map_band;
   dim3 grid((h->Hm + a.band - 1) / a.band, h->n_videos * F);
-  if (h->km == 0)
+  if (h->map_wide_img) {
+    a.band = h->map_wide_band;
+    dim3 gw((h->Hm + a.band - 1) / a.band, h->n_videos * F);
+    // measured at C3: FP64 3.3 ms per 100 frames at 1024 threads (6.5 at 256,
+    // one CTA per SM either way), FP32 2.0 ms at 256 (2.3 at 1024)
+    const int mt = h->km == 0 ? 1024 : pfk::kMapWideThreads;
+    if (h->km == 0)
+      pfk::pf_map_wide_img<double><<<gw, mt, h->map_wide_smem, h->stream>>>(a);
+    else
+      pfk::pf_map_wide_img<float><<<gw, mt, h->map_wide_smem, h->stream>>>(a);
+  } else if (h->km == 0)
     pfk::pf_map_wide<double><<<grid, 256, h->map_smem, h->stream>>>(a);
   else if (h->km == 1)
     pfk::pf_map_wide<float><<<grid, 256, h->map_smem, h->stream>>>(a);

@@ -217,6 +217,107 @@ __global__ void pf_map_wide(MapArgs a) {
   }
 }
 
+// FP32 / FP64 map through a padded term image (templates of <= 128 offsets:
+// one NumPy pairwise leaf).  The CTA expands its band of clamped source rows
+// once into term values (rows my0-2r .. my1-1, columns -2r .. W+2r-1 with
+// replicated edges), so every tap is one shared load at a per-offset
+// constant displacement and one add -- no clamps, no byte-then-term double
+// lookup, no local-memory term array (pf_map_wide).  Two map entries per
+// thread share each displacement load.  Same pairwise order, same sums.
+struct MapWideGeom {
+  int band, Wp, rows;
+  size_t smem;
+};
+__host__ __device__ inline MapWideGeom map_wide_geom(int W, int r, int n_off, int rs, int band) {
+  MapWideGeom g;
+  g.band = band;
+  g.Wp = W + 4 * r;
+  g.rows = band + 2 * r;
+  g.smem = 256 * (size_t)rs + (((size_t)n_off * 4 + 15) & ~(size_t)15) + (size_t)g.rows * g.Wp * rs;
+  return g;
+}
+constexpr int kMapWideThreads = 256;
+
+template <typename real>
+__device__ __forceinline__ void leaf_pair(const real* b0, const real* b1, const int* toff, int n, real& s0,
+                                          real& s1) {
+  if (n < 8) {
+    s0 = (real)0;
+    s1 = (real)0;
+    for (int j = 0; j < n; ++j) {
+      const int o = toff[j];
+      s0 = s0 + b0[o];
+      s1 = s1 + b1[o];
+    }
+    return;
+  }
+  real r0[8], r1[8];
+#pragma unroll
+  for (int q = 0; q < 8; ++q) {
+    const int o = toff[q];
+    r0[q] = b0[o];
+    r1[q] = b1[o];
+  }
+  int j = 8;
+  const int lim = n - (n % 8);
+  for (; j < lim; j += 8) {
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const int o = toff[j + q];
+      r0[q] = r0[q] + b0[o];
+      r1[q] = r1[q] + b1[o];
+    }
+  }
+  s0 = ((r0[0] + r0[1]) + (r0[2] + r0[3])) + ((r0[4] + r0[5]) + (r0[6] + r0[7]));
+  s1 = ((r1[0] + r1[1]) + (r1[2] + r1[3])) + ((r1[4] + r1[5]) + (r1[6] + r1[7]));
+  for (; j < n; ++j) {
+    const int o = toff[j];
+    s0 = s0 + b0[o];
+    s1 = s1 + b1[o];
+  }
+}
+
+template <typename real>
+__global__ void __launch_bounds__(1024) pf_map_wide_img(MapArgs a) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const MapWideGeom g = map_wide_geom(a.W, a.r, a.n_off, (int)sizeof(real), a.band);
+  real* term = reinterpret_cast<real*>(smem);
+  int* toff = reinterpret_cast<int*>(term + 256);
+  real* img = reinterpret_cast<real*>(reinterpret_cast<unsigned char*>(toff) + (((size_t)a.n_off * 4 + 15) & ~(size_t)15));
+  const int vf = blockIdx.y;
+  const int my0 = blockIdx.x * g.band;
+  const int my1 = min(a.Hm, my0 + g.band);
+  const int r = a.r;
+  const uint8_t* frame = a.frames + (size_t)vf * a.H * a.W;
+  const real bg = (real)a.bg, fg = (real)a.fg;
+  for (int i = threadIdx.x; i < 256; i += blockDim.x) term[i] = term_wide<real>(i, bg, fg);
+  for (int i = threadIdx.x; i < a.n_off; i += blockDim.x) {
+    const int2 o = a.offsets[i];
+    toff[i] = (o.y + r) * g.Wp + o.x + r;
+  }
+  __syncthreads();
+  const int nrow = (my1 - my0) + 2 * r;
+  for (int e = threadIdx.x; e < nrow * g.Wp; e += blockDim.x) {
+    const int ry = e / g.Wp, cx = e - ry * g.Wp;
+    const int yy = min(max(my0 - 2 * r + ry, 0), a.H - 1);
+    const int xx = min(max(cx - 2 * r, 0), a.W - 1);
+    img[e] = term[__ldg(frame + (size_t)yy * a.W + xx)];
+  }
+  __syncthreads();
+  real* out = reinterpret_cast<real*>(a.maps) + (size_t)vf * a.Hm * a.Wm;
+  const real denom = (real)a.denom;
+  const int n_e = (my1 - my0) * a.Wm;
+  for (int e0 = threadIdx.x; e0 < n_e; e0 += 2 * blockDim.x) {
+    const int e1 = min(e0 + (int)blockDim.x, n_e - 1);  // duplicate the last entry when odd
+    const int y0 = e0 / a.Wm, x0 = e0 - y0 * a.Wm;
+    const int y1 = e1 / a.Wm, x1 = e1 - y1 * a.Wm;
+    real s0, s1;
+    leaf_pair<real>(img + y0 * g.Wp + x0, img + y1 * g.Wp + x1, toff, a.n_off, s0, s1);
+    out[(size_t)(my0 + y0) * a.Wm + x0] = s0 / denom;
+    if (e0 + (int)blockDim.x < n_e) out[(size_t)(my0 + y1) * a.Wm + x1] = s1 / denom;
+  }
+}
+
 // binary16: term16 table per intensity (model.half_term_stabilized, 7 RN16
 // ops), sequential RN16 fold in template order from +0; two adjacent map
 // entries per thread in one half2.
