@@ -2,7 +2,8 @@
 384-423 binary16): every map entry equals the oracle's reference-formula
 likelihood at that clamped rint position, bit-for-bit -- for the disk
 template, other radii, an asymmetric custom template, odd frame shapes and
-the 1024x1024 C3 frame (binary16 term-image kernel and wide kernels)."""
+the 1024x1024 C3 frame in every mode, and a template over 128 offsets
+(several NumPy pairwise leaves: the generic plan kernel)."""
 
 import numpy as np
 import pytest
@@ -65,3 +66,27 @@ def test_maps_other_templates(mode):
     got = _maps(mode, frames, template=tmpl)
     ref = _oracle(mode, frames[0], offs, rp.Params())
     assert np.array_equal(np.asarray(got[0], dtype=np.float64), np.asarray(ref, dtype=np.float64))
+
+
+@pytest.mark.parametrize("mode", ["fp32", "fp64"])
+def test_maps_c3_frame_wide(mode):
+    # 1024-wide frames: 8-row bands, FP64 on 1024-thread CTAs (pf_map_wide_img)
+    frames, _ = rp.generate_video(rp.Params(), 1, 1024, 1024, (512.0, 512.0), 42)
+    got = _maps(mode, frames)[0]
+    ref = _oracle(mode, frames[0], rp.disk_offsets(5), rp.Params())
+    assert np.array_equal(got, ref.astype(got.dtype))
+
+
+@pytest.mark.parametrize("mode", ["fp16", "fp32", "fp64"])
+def test_maps_template_over_128_offsets(mode):
+    # > 128 offsets: NumPy's pairwise sum splits into several leaves (generic
+    # pf_map_wide plan evaluation for FP32 / FP64)
+    import paper_2308_00763_b200 as pf
+
+    frames, _ = rp.generate_video(rp.Params(disk_radius=7), 2, 70, 58, (35.0, 29.0), 5)
+    offs = rp.disk_offsets(7)
+    assert len(offs) > 128
+    got = _maps(mode, frames, template=pf.disk_template(7), params=pf.ModelParams(disk_radius=7))
+    for t in range(2):
+        ref = _oracle(mode, frames[t], offs, rp.Params(disk_radius=7))
+        assert np.array_equal(np.asarray(got[t], dtype=np.float64), np.asarray(ref, dtype=np.float64))
