@@ -7,6 +7,7 @@
 // tracking path runs on the device; there is no host compute path.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <climits>
 #include <cstdlib>
 #include <cmath>
@@ -167,6 +168,11 @@ struct pf_handle {
   int2* d_offs = nullptr;
   short* d_plan = nullptr;
   short2* d_leaves = nullptr;
+  int2* d_runs = nullptr;  // pf_map_wide_runs: row-prefix displacements per template run
+  int n_runs = 0;
+  bool map_runs = false;
+  int map_runs_band = 8;
+  size_t map_runs_smem = 0;
   int n_plan = 0;
   uint8_t* d_frames = nullptr;
   size_t frames_cap = 0;
@@ -308,7 +314,7 @@ int pf_destroy(pf_handle* h) {
   if (!h) return PF_OK;
   cudaSetDevice(h->device);
   void* ptrs[] = {h->X[0], h->X[1], h->C[0], h->C[1], h->rec_m, h->rec_S, h->rec_X, h->rec_Y, h->tab_s, h->tab_O,
-                  h->tab_invM, h->win, h->u, h->x0, h->tj, h->tt, h->tsync, h->tagg, h->troots, h->exp16, h->zig, h->d_offs, h->d_plan, h->d_leaves, h->d_frames,
+                  h->tab_invM, h->win, h->u, h->x0, h->tj, h->tt, h->tsync, h->tagg, h->troots, h->exp16, h->zig, h->d_offs, h->d_plan, h->d_leaves, h->d_runs, h->d_frames,
                   h->d_maps, h->d_traj, h->d_degen, h->dbg_anc, h->dbg_L, h->d_trace};
   for (void* p : ptrs)
     if (p) cudaFree(p);
@@ -574,6 +580,51 @@ static int create_impl(pf_handle** out, const pf_config* cfg, int n_shards, int 
                 "map smem attr"));
     }
   }
+  // FP32 / FP64 with integral means and a small enough template: every term
+  // and partial sum is an exact integer, so the map comes from integer row
+  // prefix sums over the template's horizontal runs (pf_map_wide_runs)
+  if (h->km != 2 && std::getenv("PF_MAP_GENERIC") == nullptr) {
+    const double bg = h->params.bg_mean, fg = h->params.fg_mean;
+    bool ok = bg == std::floor(bg) && fg == std::floor(fg) && std::fabs(bg) <= 1024 && std::fabs(fg) <= 1024;
+    long long T = 0;
+    if (ok)
+      for (int v = 0; v < 256; ++v) {
+        const long long ib = (long long)bg, ifg = (long long)fg;
+        T = std::max(T, std::llabs((v - ib) * (v - ib) - (v - ifg) * (v - ifg)));
+      }
+    ok = ok && (long long)h->n_off * T < (1LL << 24);
+    std::vector<std::pair<int, int>> so(h->n_off);
+    for (int i = 0; i < h->n_off; ++i) so[i] = {cfg->offsets_xy[2 * i + 1], cfg->offsets_xy[2 * i]};  // (dy, dx)
+    std::sort(so.begin(), so.end());
+    for (int i = 1; i < h->n_off && ok; ++i) ok = so[i] != so[i - 1];  // a multiset is not a union of runs
+    const int Wz = h->W + 4 * h->r + 1;
+    ok = ok && (long long)Wz * T < (1LL << 31);
+    if (ok) {
+      std::vector<int2> runs;
+      for (int i = 0; i < h->n_off;) {
+        int j = i;
+        while (j + 1 < h->n_off && so[j + 1].first == so[i].first && so[j + 1].second == so[j].second + 1) ++j;
+        const int dy = so[i].first, dx0 = so[i].second, dx1 = so[j].second;
+        runs.push_back(make_int2((dy + h->r) * Wz + h->r + dx1 + 1, (dy + h->r) * Wz + h->r + dx0));
+        i = j + 1;
+      }
+      int band = h->W >= 512 ? 8 : 32;
+      while (band > 1 && pfk::map_runs_geom(h->W, h->r, (int)runs.size(), band).smem > 200 * 1024) band /= 2;
+      const pfk::MapRunsGeom g = pfk::map_runs_geom(h->W, h->r, (int)runs.size(), band);
+      if (g.smem <= 200 * 1024) {
+        h->n_runs = (int)runs.size();
+        CK(cudack(cudaMalloc(&h->d_runs, runs.size() * sizeof(int2)), "runs"));
+        CK(cudack(cudaMemcpy(h->d_runs, runs.data(), runs.size() * sizeof(int2), cudaMemcpyHostToDevice), "runs"));
+        h->map_runs = true;
+        h->map_runs_band = band;
+        h->map_runs_smem = g.smem;
+        CK(cudack(cudaFuncSetAttribute(h->km == 0 ? (const void*)pfk::pf_map_wide_runs<double>
+                                                  : (const void*)pfk::pf_map_wide_runs<float>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)g.smem),
+                  "map smem attr"));
+      }
+    }
+  }
   if (h->map_smem > 48 * 1024) {
     cudaError_t ce = cudaSuccess;
     if (h->km == 0)
@@ -676,7 +727,17 @@ static int launch_maps(pf_handle* h, const uint8_t* dframes, int F) {
   a.maps = h->d_maps;
   a.band = h->map_band;
   dim3 grid((h->Hm + a.band - 1) / a.band, h->n_videos * F);
-  if (h->map_wide_img) {
+  if (h->map_runs) {
+    a.band = h->map_runs_band;
+    a.runs = h->d_runs;
+    a.n_runs = h->n_runs;
+    dim3 gw((h->Hm + a.band - 1) / a.band, h->n_videos * F);
+    // C3, 100 frames: 1.2 ms at 512-1024 threads (1.6 at 256) in both modes
+    if (h->km == 0)
+      pfk::pf_map_wide_runs<double><<<gw, 1024, h->map_runs_smem, h->stream>>>(a);
+    else
+      pfk::pf_map_wide_runs<float><<<gw, 1024, h->map_runs_smem, h->stream>>>(a);
+  } else if (h->map_wide_img) {
     a.band = h->map_wide_band;
     dim3 gw((h->Hm + a.band - 1) / a.band, h->n_videos * F);
     // measured at C3: FP64 3.3 ms per 100 frames at 1024 threads (6.5 at 256,

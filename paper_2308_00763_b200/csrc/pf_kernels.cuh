@@ -117,6 +117,8 @@ struct MapArgs {
   unsigned short bg16, fg16, s16;  // binary16 constants
   void* maps;             // [n_videos][F][Hm][Wm]
   int band;               // map rows per CTA
+  const int2* runs;       // pf_map_wide_runs: per horizontal run, row-prefix displacements (end, start)
+  int n_runs;
 };
 
 // NumPy pairwise_sum leaf (n <= 128): 8 accumulators, then tail.
@@ -315,6 +317,93 @@ __global__ void __launch_bounds__(1024) pf_map_wide_img(MapArgs a) {
     leaf_pair<real>(img + y0 * g.Wp + x0, img + y1 * g.Wp + x1, toff, a.n_off, s0, s1);
     out[(size_t)(my0 + y0) * a.Wm + x0] = s0 / denom;
     if (e0 + (int)blockDim.x < n_e) out[(size_t)(my0 + y1) * a.Wm + x1] = s1 / denom;
+  }
+}
+
+// FP32 / FP64 map from integer row prefix sums.  With integral background /
+// foreground means every term (v-bg)^2 - (v-fg)^2 is an integer and, when
+// N * max|term| < 2^24, every partial sum of the reference's pairwise order
+// is exact in FP32 and FP64 -- the sum is the same integer in any order
+// (SURVEY 8a a7).  The CTA builds int32 term rows for its band, prefix-sums
+// each row (one warp per row), and evaluates the template as horizontal runs
+// (dy, dx0..dx1): two shared loads per run instead of one per offset (the
+// r = 5 disk: 11 runs for 81 offsets).  The host picks this kernel only when
+// the exactness conditions hold (pf_api.cu), else pf_map_wide_img.
+struct MapRunsGeom {
+  int band, Wz, rows;
+  size_t smem;
+};
+__host__ __device__ inline MapRunsGeom map_runs_geom(int W, int r, int n_runs, int band) {
+  MapRunsGeom g;
+  g.band = band;
+  g.Wz = W + 4 * r + 1;
+  g.rows = band + 2 * r;
+  g.smem = 256 * 4 + (size_t)n_runs * 8 + (size_t)g.rows * g.Wz * 4;
+  return g;
+}
+
+template <typename real>
+__global__ void __launch_bounds__(1024) pf_map_wide_runs(MapArgs a) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const MapRunsGeom g = map_runs_geom(a.W, a.r, a.n_runs, a.band);
+  int* term = reinterpret_cast<int*>(smem);
+  int2* runs = reinterpret_cast<int2*>(term + 256);
+  int* pz = reinterpret_cast<int*>(runs + a.n_runs);
+  const int vf = blockIdx.y;
+  const int my0 = blockIdx.x * g.band;
+  const int my1 = min(a.Hm, my0 + g.band);
+  const int r = a.r;
+  const uint8_t* frame = a.frames + (size_t)vf * a.H * a.W;
+  const int ibg = (int)a.bg, ifg = (int)a.fg;
+  for (int i = threadIdx.x; i < 256; i += blockDim.x) term[i] = (i - ibg) * (i - ibg) - (i - ifg) * (i - ifg);
+  for (int i = threadIdx.x; i < a.n_runs; i += blockDim.x) runs[i] = a.runs[i];
+  __syncthreads();
+  const int nrow = (my1 - my0) + 2 * r, Wp = g.Wz - 1;
+  for (int e = threadIdx.x; e < nrow * Wp; e += blockDim.x) {
+    const int ry = e / Wp, cx = e - ry * Wp;
+    const int yy = min(max(my0 - 2 * r + ry, 0), a.H - 1);
+    const int xx = min(max(cx - 2 * r, 0), a.W - 1);
+    pz[ry * g.Wz + cx + 1] = term[__ldg(frame + (size_t)yy * a.W + xx)];
+  }
+  __syncthreads();
+  {  // inclusive prefix sum of every row, one warp per row
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    for (int ry = wid; ry < nrow; ry += nw) {
+      int* row = pz + ry * g.Wz;
+      int carry = 0;
+      for (int c0 = 1; c0 < g.Wz; c0 += 32) {
+        const int c = c0 + lane;
+        int v = c < g.Wz ? row[c] : 0;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const int t = __shfl_up_sync(0xffffffffu, v, o);
+          if (lane >= o) v += t;
+        }
+        v += carry;
+        if (c < g.Wz) row[c] = v;
+        carry = __shfl_sync(0xffffffffu, v, 31);
+      }
+      if (lane == 0) row[0] = 0;
+    }
+  }
+  __syncthreads();
+  real* out = reinterpret_cast<real*>(a.maps) + (size_t)vf * a.Hm * a.Wm;
+  const real denom = (real)a.denom;
+  const int n_e = (my1 - my0) * a.Wm;
+  for (int e0 = threadIdx.x; e0 < n_e; e0 += 2 * blockDim.x) {
+    const int e1 = min(e0 + (int)blockDim.x, n_e - 1);
+    const int y0 = e0 / a.Wm, x0 = e0 - y0 * a.Wm;
+    const int y1 = e1 / a.Wm, x1 = e1 - y1 * a.Wm;
+    const int* b0 = pz + y0 * g.Wz + x0;
+    const int* b1 = pz + y1 * g.Wz + x1;
+    int s0 = 0, s1 = 0;
+    for (int j = 0; j < a.n_runs; ++j) {
+      const int2 d = runs[j];
+      s0 += b0[d.x] - b0[d.y];
+      s1 += b1[d.x] - b1[d.y];
+    }
+    out[(size_t)(my0 + y0) * a.Wm + x0] = (real)s0 / denom;
+    if (e0 + (int)blockDim.x < n_e) out[(size_t)(my0 + y1) * a.Wm + x1] = (real)s1 / denom;
   }
 }
 

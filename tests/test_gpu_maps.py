@@ -90,3 +90,29 @@ def test_maps_template_over_128_offsets(mode):
     for t in range(2):
         ref = _oracle(mode, frames[t], offs, rp.Params(disk_radius=7))
         assert np.array_equal(np.asarray(got[t], dtype=np.float64), np.asarray(ref, dtype=np.float64))
+
+
+@pytest.mark.parametrize("mode", ["fp32", "fp64"])
+@pytest.mark.parametrize("bg,fg,scale", [(100.0, 228.0, 37.5), (99.5, 230.25, 50.0), (-3.0, 1000.0, 50.0)])
+def test_maps_params_integer_and_fractional_means(mode, bg, fg, scale):
+    # integral means within the exactness bound: integer row-prefix kernel;
+    # fractional means (or terms too large): the term-image kernel
+    import paper_2308_00763_b200 as pf
+
+    frames, _ = rp.generate_video(rp.Params(), 2, 83, 41, (40.0, 20.0), 9)
+    got = _maps(mode, frames, params=pf.ModelParams(bg_mean=bg, fg_mean=fg, likelihood_scale=scale))
+    for t in range(2):
+        ref = _oracle(mode, frames[t], rp.disk_offsets(5), rp.Params(bg_mean=bg, fg_mean=fg, likelihood_scale=scale))
+        assert np.array_equal(got[t], ref.astype(got.dtype))
+
+
+@pytest.mark.parametrize("mode", ["fp32", "fp64"])
+def test_maps_duplicate_offsets(mode):
+    # a template with a repeated offset is a multiset, not a union of runs
+    import paper_2308_00763_b200 as pf
+
+    frames, _ = rp.generate_video(rp.Params(), 1, 64, 48, (30.0, 20.0), 4)
+    offs = np.array([[0, 0], [1, 0], [1, 0], [2, 0], [-1, 2], [0, 2]], dtype=np.int64)
+    got = _maps(mode, frames, template=pf.PixelTemplate(offs))
+    ref = _oracle(mode, frames[0], offs, rp.Params())
+    assert np.array_equal(got[0], ref.astype(got.dtype))
