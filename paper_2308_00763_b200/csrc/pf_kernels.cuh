@@ -1761,6 +1761,19 @@ __device__ __forceinline__ void scatter_windows(const WinShards& w, size_t track
   for (long long d = first_hi(sb), e = first_hi(sn); d < e; ++d) rec(d)->y = b;
 }
 
+// scatter_windows for one unsharded track (the tile table): 32-bit indices,
+// shifts for the non-negative tile divisions, direct record pointer
+__device__ __forceinline__ void scatter_windows_local(int2* wr, int n, long long K, int b, long long sb,
+                                                      long long sn) {
+  static_assert(PF_TILE == 1024, "tile shift");
+  const int dl = (int)min((long long)n, (sb + PF_TILE - 1) >> 10);
+  const int el = (int)min((long long)n, (sn + PF_TILE - 1) >> 10);
+  const int dh = sb >= K ? n : (int)min((long long)n - 1, sb >> 10);
+  const int eh = sn >= K ? n : (int)min((long long)n - 1, sn >> 10);
+  for (int d = dl; d < el; ++d) wr[d].x = b;
+  for (int d = dh; d < eh; ++d) wr[d].y = b;
+}
+
 // Tile table, one CTA per chunk of blockDim.x tiles (one tile per thread),
 // grid (n_chunks, n_tracks).  All cross-CTA combination is exact: the global
 // max is an atomicMax over order-preserving keys, the mass prefix an int64
@@ -1901,11 +1914,7 @@ __global__ void __launch_bounds__(1024) pf_tile_table(TableArgs a) {
       while (k < a.K && point_of<MODE>(k, u, a.K, invK) <= On) ++k;
       sn = k;
     }
-    WinShards ws;
-    ws.n_shards = 1;
-    ws.shard_tiles = n;
-    ws.win[0] = a.win;
-    scatter_windows(ws, (size_t)track * n, n, a.K, b, sb, sn);
+    scatter_windows_local(a.win + (size_t)track * n, n, a.K, b, sb, sn);
   }
   // early release of the next frame: table entries, windows and u are
   // published with a per-track monotone counter (sy[1], +1 per chunk); the
