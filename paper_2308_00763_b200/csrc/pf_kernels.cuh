@@ -1799,6 +1799,9 @@ __global__ void __launch_bounds__(1024) pf_tile_table(TableArgs a) {
   pdl_launch_dependents();
   // the frame's resampling uniform: stream position t(2K+1)+2K
   const double u = pfr::uniform_of(a.ua * a.x0[track] + a.uc);
+  const double scale = ldexp(1.0, a.Q - FB);
+  const double Kd = __ll2double_rn(a.K);
+  const double invK = __ddiv_rn(1.0, Kd);
   pdl_wait();  // tile records of this frame's fused kernel
   PF_TRACE(a, 1);
   const size_t rb = (size_t)track * n + (valid ? b : 0);
@@ -1809,9 +1812,6 @@ __global__ void __launch_bounds__(1024) pf_tile_table(TableArgs a) {
   //    maxima into sy[0] (order keys); reset by the last reader below
   const double m = okey_inv(__ldcg(sy + 0));
   PF_TRACE(a, 4);
-  const double scale = ldexp(1.0, a.Q - FB);
-  const double Kd = __ll2double_rn(a.K);
-  const double invK = __ddiv_rn(1.0, Kd);
 
   // 2. exact fixed-point tile mass and its prefix across the chunk / track
   double f = 0.0;
