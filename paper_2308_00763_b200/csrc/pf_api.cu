@@ -135,6 +135,10 @@ int next_pow2(long long v) {
 
 }  // namespace
 
+// host frames are uploaded in this many chunks on a copy stream; each
+// chunk's likelihood maps start as soon as it lands (pf_run)
+constexpr int kUploadChunks = 8;
+
 struct pf_handle {
   int precision = 0, km = 0;
   long long K = 0;
@@ -187,6 +191,8 @@ struct pf_handle {
   long long frame_counter = 0;
   std::string err;
   cudaEvent_t ev[6] = {};
+  cudaStream_t cstream = nullptr;          // host-frame uploads, chunked ahead of the maps
+  cudaEvent_t cev[kUploadChunks] = {};     // per-chunk upload done
   float timings[6] = {0};
   int64_t launches = 0;
   int degenerate_frame = -1;
@@ -330,6 +336,9 @@ int pf_destroy(pf_handle* h) {
   for (auto& e : h->ev)
     if (e) cudaEventDestroy(e);
   for (auto& e : h->pev) cudaEventDestroy(e);
+  for (auto& e : h->cev)
+    if (e) cudaEventDestroy(e);
+  if (h->cstream) cudaStreamDestroy(h->cstream);
   if (h->gexec) cudaGraphExecDestroy(h->gexec);
   if (h->stream) cudaStreamDestroy(h->stream);
   delete h;
@@ -704,10 +713,13 @@ int pf_reset(pf_handle* h, double x0, double y0) {
   return PF_OK;
 }
 
-static int launch_maps(pf_handle* h, const uint8_t* dframes, int F) {
+// maps of frames [f0, f0 + nf) of a one-video buffer of F frames (nf < 0: all)
+static int launch_maps(pf_handle* h, const uint8_t* dframes, int F, int f0 = 0, int nf = -1) {
+  if (nf < 0) nf = F;
+  if (h->n_videos != 1 && (f0 != 0 || nf != F)) return PF_EINVAL;
   pfk::MapArgs a{};
-  a.frames = dframes;
-  a.n_frames = F;
+  a.frames = dframes + (size_t)f0 * h->H * h->W;
+  a.n_frames = nf;
   a.H = h->H;
   a.W = h->W;
   a.r = h->r;
@@ -724,14 +736,14 @@ static int launch_maps(pf_handle* h, const uint8_t* dframes, int F) {
   a.bg16 = f64_to_f16(h->params.bg_mean);
   a.fg16 = f64_to_f16(h->params.fg_mean);
   a.s16 = f64_to_f16(1.0 / std::sqrt(h->params.likelihood_scale * h->n_off));
-  a.maps = h->d_maps;
+  a.maps = (char*)h->d_maps + (size_t)f0 * h->Hm * h->Wm * h->rs;
   a.band = h->map_band;
-  dim3 grid((h->Hm + a.band - 1) / a.band, h->n_videos * F);
+  dim3 grid((h->Hm + a.band - 1) / a.band, h->n_videos * nf);
   if (h->map_runs) {
     a.band = h->map_runs_band;
     a.runs = h->d_runs;
     a.n_runs = h->n_runs;
-    dim3 gw((h->Hm + a.band - 1) / a.band, h->n_videos * F);
+    dim3 gw((h->Hm + a.band - 1) / a.band, h->n_videos * nf);
     // C3, 100 frames: 1.2 ms at 512-1024 threads (1.6 at 256) in both modes
     if (h->km == 0)
       pfk::pf_map_wide_runs<double><<<gw, 1024, h->map_runs_smem, h->stream>>>(a);
@@ -739,7 +751,7 @@ static int launch_maps(pf_handle* h, const uint8_t* dframes, int F) {
       pfk::pf_map_wide_runs<float><<<gw, 1024, h->map_runs_smem, h->stream>>>(a);
   } else if (h->map_wide_img) {
     a.band = h->map_wide_band;
-    dim3 gw((h->Hm + a.band - 1) / a.band, h->n_videos * F);
+    dim3 gw((h->Hm + a.band - 1) / a.band, h->n_videos * nf);
     // measured at C3: FP64 3.3 ms per 100 frames at 1024 threads (6.5 at 256,
     // one CTA per SM either way), FP32 2.0 ms at 256 (2.3 at 1024)
     const int mt = h->km == 0 ? 1024 : pfk::kMapWideThreads;
@@ -753,7 +765,7 @@ static int launch_maps(pf_handle* h, const uint8_t* dframes, int F) {
     pfk::pf_map_wide<float><<<grid, 256, h->map_smem, h->stream>>>(a);
   else if (h->map_img) {
     const pfk::MapHalfGeom g = pfk::map_half_geom(h->W, h->H, h->r, h->n_off);
-    dim3 gi((h->Hm + g.band - 1) / g.band, h->n_videos * F);
+    dim3 gi((h->Hm + g.band - 1) / g.band, h->n_videos * nf);
     if (h->precision == PF_FP16)  // scalar lanes ("fp16")
       pfk::pf_map_half_img<false><<<gi, pfk::kMapHalfThreads, g.smem, h->stream>>>(a);
     else
@@ -932,10 +944,36 @@ int pf_run(pf_handle* h, const uint8_t* frames, int32_t F, int32_t on_device, do
     dframes = h->d_frames;
   }
   PF_CUDA(cudaEventRecord(h->ev[0], h->stream), h->err);
-  if (!on_device)
-    PF_CUDA(cudaMemcpyAsync(h->d_frames, frames, fbytes, cudaMemcpyHostToDevice, h->stream), h->err);
-  PF_CUDA(cudaEventRecord(h->ev[1], h->stream), h->err);
-  if ((rc = launch_maps(h, dframes, F))) return rc;
+  // (C3's 100 MB: 31.4 -> 30.0 ms per step; below ~8 MB the extra map launches
+  // cost more than the upload they hide -- C2's 1.6 MB: +0.1 ms)
+  if (!on_device && h->n_videos == 1 && F >= kUploadChunks && fbytes >= (8u << 20)) {
+    // chunked upload on the copy stream; each chunk's maps start when it lands
+    // ("upload" then times only the exposed first chunk)
+    if (!h->cstream) {
+      PF_CUDA(cudaStreamCreateWithFlags(&h->cstream, cudaStreamNonBlocking), h->err);
+      for (auto& e : h->cev) PF_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), h->err);
+    }
+    PF_CUDA(cudaStreamWaitEvent(h->cstream, h->ev[0], 0), h->err);  // earlier readers of d_frames
+    const size_t fb = (size_t)h->H * h->W;
+    const int per = (F + kUploadChunks - 1) / kUploadChunks;
+    for (int c = 0; c * per < F; ++c) {
+      const int f0 = c * per, nf = std::min(per, F - f0);
+      PF_CUDA(cudaMemcpyAsync(h->d_frames + f0 * fb, frames + f0 * fb, nf * fb, cudaMemcpyHostToDevice, h->cstream),
+              h->err);
+      PF_CUDA(cudaEventRecord(h->cev[c], h->cstream), h->err);
+    }
+    for (int c = 0; c * per < F; ++c) {
+      const int f0 = c * per, nf = std::min(per, F - f0);
+      PF_CUDA(cudaStreamWaitEvent(h->stream, h->cev[c], 0), h->err);
+      if (c == 0) PF_CUDA(cudaEventRecord(h->ev[1], h->stream), h->err);
+      if ((rc = launch_maps(h, dframes, F, f0, nf))) return rc;
+    }
+  } else {
+    if (!on_device)
+      PF_CUDA(cudaMemcpyAsync(h->d_frames, frames, fbytes, cudaMemcpyHostToDevice, h->stream), h->err);
+    PF_CUDA(cudaEventRecord(h->ev[1], h->stream), h->err);
+    if ((rc = launch_maps(h, dframes, F))) return rc;
+  }
   PF_CUDA(cudaEventRecord(h->ev[2], h->stream), h->err);
   const long long vstride = (long long)F * map_elems;  // elements between videos
   const bool graph_ok = h->use_graphs && !h->profiling && F >= 4;

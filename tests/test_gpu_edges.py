@@ -54,3 +54,24 @@ def test_asymmetric_template_fused():
         got = pf.Filter(5000, mode, 64, 64, 4, template=pf.PixelTemplate(offs)).run(frames)
         ref, _ = fused.run(frames, 5000, mode, 4, offsets=offs)
         assert np.array_equal(got, ref), mode
+
+
+@pytest.mark.parametrize("mode", ["fp16-packed", "fp64"])
+@pytest.mark.parametrize("W,F", [(512, 43), (384, 100)])
+def test_chunked_host_upload_equals_device_frames(mode, W, F):
+    # host frames of >= 8 MB are uploaded in chunks on a copy stream with each
+    # chunk's maps started as it lands: same trajectory as device-resident frames
+    import torch
+
+    import paper_2308_00763_b200 as pf
+
+    frames, _ = rp.generate_video(rp.Params(), F, W, W, (W / 2.0, W / 2.0), 42)
+    assert frames.nbytes >= 8 << 20
+    f = pf.Filter(20_000, mode, W, W, 42)
+    dev = f.run_frames(torch.from_numpy(frames).cuda(), F)
+    f.reset()
+    host = f.run_frames(frames, F)
+    f.reset()
+    pinned = f.run_frames(torch.from_numpy(frames).pin_memory().numpy(), F)
+    f.close()
+    assert np.array_equal(dev, host) and np.array_equal(dev, pinned)
