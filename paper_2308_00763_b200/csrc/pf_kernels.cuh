@@ -1352,11 +1352,6 @@ __global__ void __launch_bounds__(PF_TILE / (VPT * R), fused_min_blocks<MODE>(PF
   }
   const double invK = __ddiv_rn(1.0, (double)K);
 
-  auto tab_s = [&](int b) -> int { return staged ? s_ts[b - b_lo] : g_ts(b); };
-  auto tab_O = [&](int b) -> double { return staged ? s_tO[b - b_lo] : g_tO(b); };
-  auto tab_M = [&](int b) -> double { return staged ? s_tM[b - b_lo] : g_tM(b); };
-  // a source tile's local CDF: staged copy in shared memory, else its shard's buffer
-  auto tile_C = [&](int b) -> const real* { return staged ? s_c + (b - b_lo) * PF_TILE : src_C(b); };
 
   // ---- phase 1: resample + propagate + likelihood -------------------------
   // Threads whose VPT particles all lie inside the tile (all but at most one
@@ -1378,62 +1373,84 @@ __global__ void __launch_bounds__(PF_TILE / (VPT * R), fused_min_blocks<MODE>(PF
 #pragma unroll
         for (int i = 0; i < VPT; ++i) anc[i] = base + l0 + i;
       } else {
-        int b = b_lo;
-        if (!staged) {
-          int lo = b_lo, hi = b_hi;
-          while (lo < hi) {
-            const int mid = (lo + hi + 1) >> 1;
-            if (g_ts(mid) <= base + l0)
-              lo = mid;
-            else
-              hi = mid - 1;
+        // the search runs in two instantiations: window staged in shared
+        // memory (the common case: LDS through shared-typed pointers) or
+        // read from the source tiles' buffers (global loads)
+        auto resample = [&](auto st_tag) {
+          constexpr bool ST = decltype(st_tag)::value;
+          auto tsv = [&](int b) -> int {
+            if constexpr (ST) return s_ts[b - b_lo]; else return g_ts(b);
+          };
+          auto tOv = [&](int b) -> double {
+            if constexpr (ST) return s_tO[b - b_lo]; else return g_tO(b);
+          };
+          auto tMv = [&](int b) -> double {
+            if constexpr (ST) return s_tM[b - b_lo]; else return g_tM(b);
+          };
+          auto tCv = [&](int b) -> const real* {
+            if constexpr (ST) return s_c + (b - b_lo) * PF_TILE; else return src_C(b);
+          };
+          int b = b_lo;
+          if constexpr (!ST) {
+            int lo = b_lo, hi = b_hi;
+            while (lo < hi) {
+              const int mid = (lo + hi + 1) >> 1;
+              if (g_ts(mid) <= base + l0)
+                lo = mid;
+              else
+                hi = mid - 1;
+            }
+            b = lo;
           }
-          b = lo;
-        }
-        // register-cached geometry of the current source tile
-        int sb = tab_s(b), snext = b < b_hi ? tab_s(b + 1) : K;
-        double gO = tab_O(b), gM = tab_M(b);
-        float fO = (float)gO, fM = (float)gM;  // FP16: the table holds f32 values
-        int tl = b * PF_TILE, tb = min(PF_TILE, K - tl);
-        const real* cb = tile_C(b);
-        int jprev = -1;
-#pragma unroll
-        for (int i = 0; i < VPT; ++i) {
-          const int k = base + l0 + i;
-          if (!FULL && k >= K) {
-            anc[i] = k;
-            continue;
+          // register-cached geometry of the current source tile
+          int sb = tsv(b), snext = b < b_hi ? tsv(b + 1) : K;
+          double gO = tOv(b), gM = tMv(b);
+          float fO = (float)gO, fM = (float)gM;  // FP16: the table holds f32 values
+          int tl = b * PF_TILE, tb = min(PF_TILE, K - tl);
+          const real* cb = tCv(b);
+          int jprev = -1;
+  #pragma unroll
+          for (int i = 0; i < VPT; ++i) {
+            const int k = base + l0 + i;
+            if (!FULL && k >= K) {
+              anc[i] = k;
+              continue;
+            }
+            if (k >= snext) {  // next source tile (rare: outputs of one source tile are contiguous)
+              do {
+                ++b;
+                snext = b < b_hi ? tsv(b + 1) : K;
+              } while (k >= snext);
+              sb = tsv(b);
+              gO = tOv(b);
+              gM = tMv(b);
+              fO = (float)gO;
+              fM = (float)gM;
+              tl = b * PF_TILE;
+              tb = min(PF_TILE, K - tl);
+              cb = tCv(b);
+              jprev = -1;
+            }
+            typename KT::k_t kq;
+            if constexpr (MODE == M_FP16) {
+              // f32 tile-local point: q = ((k - s_b) + phi_b) * rho_b
+              const float qf = __fmul_rn(__fadd_rn((float)(k - sb), fO), fM);
+              kq = __half_as_ushort(__float2half_ru(fminf(fmaxf(qf, 0.0f), 1.0f)));
+            } else {
+              const double p = point_of<MODE>(k, u, K, invK);
+              const double q = gM == 0.0 ? 0.0 : __dmul_rn(__dsub_rn(p, gO), gM);
+              kq = KT::up(fmin(fmax(q, 0.0), 1.0));
+            }
+            int j = jprev >= 0 ? advance_key<MODE>(cb, jprev, tb, kq) : lb_branchless<MODE>(cb, tb, kq);
+            j = min(j, tb - 1);
+            jprev = j;
+            anc[i] = tl + j;
           }
-          if (k >= snext) {  // next source tile (rare: outputs of one source tile are contiguous)
-            do {
-              ++b;
-              snext = b < b_hi ? tab_s(b + 1) : K;
-            } while (k >= snext);
-            sb = tab_s(b);
-            gO = tab_O(b);
-            gM = tab_M(b);
-            fO = (float)gO;
-            fM = (float)gM;
-            tl = b * PF_TILE;
-            tb = min(PF_TILE, K - tl);
-            cb = tile_C(b);
-            jprev = -1;
-          }
-          typename KT::k_t kq;
-          if constexpr (MODE == M_FP16) {
-            // f32 tile-local point: q = ((k - s_b) + phi_b) * rho_b
-            const float qf = __fmul_rn(__fadd_rn((float)(k - sb), fO), fM);
-            kq = __half_as_ushort(__float2half_ru(fminf(fmaxf(qf, 0.0f), 1.0f)));
-          } else {
-            const double p = point_of<MODE>(k, u, K, invK);
-            const double q = gM == 0.0 ? 0.0 : __dmul_rn(__dsub_rn(p, gO), gM);
-            kq = KT::up(fmin(fmax(q, 0.0), 1.0));
-          }
-          int j = jprev >= 0 ? advance_key<MODE>(cb, jprev, tb, kq) : lb_branchless<MODE>(cb, tb, kq);
-          j = min(j, tb - 1);
-          jprev = j;
-          anc[i] = tl + j;
-        }
+        };
+        if (staged)
+          resample(std::true_type{});
+        else
+          resample(std::false_type{});
       }
       if (a.dbg_anc != nullptr) {
 #pragma unroll
