@@ -163,7 +163,9 @@ __global__ void pf_map_wide(MapArgs a) {
   int2* offs = reinterpret_cast<int2*>(smem + 16 + 256 * sizeof(real));
   short* plan = reinterpret_cast<short*>(offs + a.n_off);
   short2* leaves = reinterpret_cast<short2*>(plan + ((a.n_plan + 1) & ~1));
-  uint8_t* rows = reinterpret_cast<uint8_t*>(((uintptr_t)(leaves + a.n_plan) + 15) & ~(uintptr_t)15);
+  // byte offsets from the shared base (a uintptr_t round trip would hide the
+  // address space: generic loads instead of LDS)
+  uint8_t* rows = smem + ((reinterpret_cast<unsigned char*>(leaves + a.n_plan) - smem + 15) & ~15);
 
   const int vf = blockIdx.y;  // video * n_frames + frame
   const int my0 = blockIdx.x * a.band;
@@ -415,7 +417,7 @@ __global__ void pf_map_half(MapArgs a) {
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem);
   __half* term = reinterpret_cast<__half*>(smem + 16);
   int2* offs = reinterpret_cast<int2*>(smem + 16 + 256 * sizeof(__half));
-  uint8_t* rows = reinterpret_cast<uint8_t*>(((uintptr_t)(offs + a.n_off) + 15) & ~(uintptr_t)15);
+  uint8_t* rows = smem + ((reinterpret_cast<unsigned char*>(offs + a.n_off) - smem + 15) & ~15);
 
   const int vf = blockIdx.y;
   const int my0 = blockIdx.x * a.band;
@@ -498,7 +500,7 @@ __global__ void __launch_bounds__(kMapHalfThreads) pf_map_half_img(MapArgs a) {
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem);
   __half* term = reinterpret_cast<__half*>(smem + 16);
   int* tapw = reinterpret_cast<int*>(smem + 16 + 512);
-  uint8_t* rows = reinterpret_cast<uint8_t*>(((uintptr_t)(tapw + a.n_off) + 15) & ~(uintptr_t)15);
+  uint8_t* rows = smem + ((reinterpret_cast<unsigned char*>(tapw + a.n_off) - smem + 15) & ~15);
   const size_t frame_rows = (size_t)(g.band + 2 * a.r) * a.W + 32;
   __half* imgA = reinterpret_cast<__half*>(rows + ((frame_rows + 15) & ~(size_t)15));
   __half* imgB = imgA + (size_t)g.rows_img * g.P;
