@@ -1068,7 +1068,8 @@ __device__ __forceinline__ double tree_vpt(const double* v) {
 // registers: -9%).
 template <int MODE>
 constexpr int fused_min_blocks(int tpb) {
-  return tpb != 256 ? 0 : MODE == M_FP16 ? 7 : MODE == M_FP32 ? 6 : 5;  // 0: no constraint
+  return tpb == 128 ? (MODE == M_FP32 ? 7 : MODE == M_FP64 ? 6 : 0)
+         : tpb != 256 ? 0 : MODE == M_FP16 ? 7 : MODE == M_FP32 ? 6 : 5;  // 0: no constraint
 }
 
 // One CTA = one tile of PF_TILE particles of one track; TPB = PF_TILE/(VPT*R)
