@@ -1069,7 +1069,7 @@ __device__ __forceinline__ double tree_vpt(const double* v) {
 template <int MODE>
 constexpr int fused_min_blocks(int tpb) {
   return tpb == 128 ? (MODE == M_FP32 ? 7 : MODE == M_FP64 ? 6 : 0)
-         : tpb != 256 ? 0 : MODE == M_FP16 ? 7 : MODE == M_FP32 ? 6 : 5;  // 0: no constraint
+         : tpb != 256 ? 0 : MODE == M_FP16 ? 7 : MODE == M_FP32 ? 6 : 4;  // 0: no constraint
 }
 
 // One CTA = one tile of PF_TILE particles of one track; TPB = PF_TILE/(VPT*R)
