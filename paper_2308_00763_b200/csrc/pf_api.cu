@@ -231,15 +231,15 @@ struct pf_handle {
 
 typedef void (*fused_fn)(pfk::FusedArgs);
 // (VPT, rounds) per threads-per-block: the tile is always PF_TILE particles
-template <int M, bool PK = true>
+template <int M, bool PK = true, bool DBG = false>
 static fused_fn fused_for_tpb(int tpb) {
   switch (tpb) {
-    case 32: return pfk::pf_fused_frame<M, 8, 4, false, PK>;
-    case 64: return pfk::pf_fused_frame<M, 8, 2, false, PK>;
-    case 128: return pfk::pf_fused_frame<M, 8, 1, false, PK>;
-    case 512: return pfk::pf_fused_frame<M, 2, 1, false, PK>;
-    case 1024: return pfk::pf_fused_frame<M, 1, 1, false, PK>;
-    default: return pfk::pf_fused_frame<M, 4, 1, false, PK>;
+    case 32: return pfk::pf_fused_frame<M, 8, 4, false, PK, DBG>;
+    case 64: return pfk::pf_fused_frame<M, 8, 2, false, PK, DBG>;
+    case 128: return pfk::pf_fused_frame<M, 8, 1, false, PK, DBG>;
+    case 512: return pfk::pf_fused_frame<M, 2, 1, false, PK, DBG>;
+    case 1024: return pfk::pf_fused_frame<M, 1, 1, false, PK, DBG>;
+    default: return pfk::pf_fused_frame<M, 4, 1, false, PK, DBG>;
   }
 }
 // sharded filters: 128 or 256 threads per block only (keeps the instantiations few)
@@ -247,14 +247,28 @@ template <int M>
 static fused_fn fused_sharded(int tpb) {
   return tpb == 128 ? pfk::pf_fused_frame<M, 8, 1, true> : pfk::pf_fused_frame<M, 4, 1, true>;
 }
-static fused_fn fused_kernel(const pf_handle* h) {
+// dbg: the instantiation with the trace / debug-capture hooks (pf_set_trace,
+// pf_get_debug); the production kernels carry neither
+template <bool DBG>
+static fused_fn fused_unsharded(const pf_handle* h) {
+  if (h->km == 2 && h->precision == PF_FP16) return fused_for_tpb<2, false, DBG>(h->tpb);  // scalar lanes
+  return h->km == 0 ? fused_for_tpb<0, true, DBG>(h->tpb)
+                    : h->km == 1 ? fused_for_tpb<1, true, DBG>(h->tpb) : fused_for_tpb<2, true, DBG>(h->tpb);
+}
+static bool fused_dbg(const pf_handle* h) { return h->n_shards == 1 && (h->dbg_anc != nullptr || h->tracing); }
+static fused_fn fused_kernel(const pf_handle* h, int dbg = -1) {
   if (h->n_shards > 1)
     return h->km == 0 ? fused_sharded<0>(h->tpb) : h->km == 1 ? fused_sharded<1>(h->tpb) : fused_sharded<2>(h->tpb);
-  if (h->km == 2 && h->precision == PF_FP16) return fused_for_tpb<2, false>(h->tpb);  // scalar lanes
-  return h->km == 0 ? fused_for_tpb<0>(h->tpb) : h->km == 1 ? fused_for_tpb<1>(h->tpb) : fused_for_tpb<2>(h->tpb);
+  const bool d = dbg < 0 ? fused_dbg(h) : dbg != 0;
+  return d ? fused_unsharded<true>(h) : fused_unsharded<false>(h);
 }
 static cudaError_t set_fused_smem(const pf_handle* h) {
-  return cudaFuncSetAttribute(fused_kernel(h), cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->fused_smem);
+  cudaError_t e = cudaFuncSetAttribute((const void*)fused_kernel(h, 0), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)h->fused_smem);
+  if (e == cudaSuccess && h->n_shards == 1)
+    e = cudaFuncSetAttribute((const void*)fused_kernel(h, 1), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)h->fused_smem);
+  return e;
 }
 
 // launch with programmatic stream serialization (PDL): the kernel may begin

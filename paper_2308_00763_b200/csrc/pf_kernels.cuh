@@ -661,6 +661,10 @@ __device__ __forceinline__ unsigned long long gtimer() {
     if ((A).trace != nullptr && threadIdx.x == 0 && blockIdx.y == 0)        \
       (A).trace[(size_t)blockIdx.x * 8 + (SLOT)] = gtimer();                \
   } while (0)
+#define PF_TRACE_DBG(A, SLOT)   \
+  do {                          \
+    if constexpr (DBG) PF_TRACE(A, SLOT); \
+  } while (0)
 
 // order-preserving map double -> uint64 (for atomicMax); 0 is below every key
 __device__ __forceinline__ unsigned long long okey(double d) {
@@ -1076,7 +1080,10 @@ constexpr int fused_min_blocks(int tpb) {
 // threads, thread t of round r owns particles (r*TPB + t)*VPT .. +VPT-1.
 // SH: sharded filter (source tiles on several shards); PK: FP16 in packed
 // half2 lanes (false: scalar lanes, "fp16" mode -- same values)
-template <int MODE, int VPT, int R, bool SH = false, bool PK = true>
+// DBG: the %globaltimer trace and the ancestor / likelihood capture of the
+// parity tests are compiled only into this instantiation (as runtime checks
+// they cost the production kernel ~10% at C3: registers and code layout)
+template <int MODE, int VPT, int R, bool SH = false, bool PK = true, bool DBG = false>
 __global__ void __launch_bounds__(PF_TILE / (VPT * R), fused_min_blocks<MODE>(PF_TILE / (VPT * R)))
     pf_fused_frame(FusedArgs a) {
   using real = typename Tr<MODE>::real;
@@ -1159,7 +1166,7 @@ __global__ void __launch_bounds__(PF_TILE / (VPT * R), fused_min_blocks<MODE>(PF
     uint4* zdst = reinterpret_cast<uint4*>(smem);
     for (int i = tid; i < kZigBytes / 16; i += TPB) zdst[i] = zsrc[i];
   }
-  PF_TRACE(a, 0);
+  PF_TRACE_DBG(a, 0);
   if (tid == 0) s_int[3] = 0;
   // stream state at this tile's first draw, position t(2K+1) + 2*base: the
   // frame's affine jump (kernel argument) and the per-tile jump
@@ -1230,7 +1237,7 @@ __global__ void __launch_bounds__(PF_TILE / (VPT * R), fused_min_blocks<MODE>(PF
     }
   }
   __syncthreads();
-  PF_TRACE(a, 1);
+  PF_TRACE_DBG(a, 1);
   // ---- warp 0: wait for the previous kernels, read this tile's source window
   //      (written by the previous frame's tile table) and start ONE bulk copy
   //      (cp.async.bulk, mbarrier-tracked) of exactly the source tiles' local
@@ -1264,7 +1271,7 @@ __global__ void __launch_bounds__(PF_TILE / (VPT * R), fused_min_blocks<MODE>(PF
     } else {
       pdl_wait();  // frame 0: the likelihood maps / initial positions
     }
-    PF_TRACE(a, 2);
+    PF_TRACE_DBG(a, 2);
     if (a.t > 0) {
       const int2 wn = __ldcg(reinterpret_cast<const int2*>(a.win) + (size_t)track * nl + ltile);
       const int nsrc = wn.y - wn.x + 1;
@@ -1328,7 +1335,7 @@ __global__ void __launch_bounds__(PF_TILE / (VPT * R), fused_min_blocks<MODE>(PF
     }
   }
   __syncthreads();  // window and slow-path noise visible (and, for every thread, the previous table)
-  PF_TRACE(a, 3);
+  PF_TRACE_DBG(a, 3);
   const double u = a.t > 0 ? __ldcg(a.u_prev + track) : 0.0;
   int b_lo = 0, b_hi = 0, staged = 0;
   if (a.t > 0) {
@@ -1455,7 +1462,7 @@ __global__ void __launch_bounds__(PF_TILE / (VPT * R), fused_min_blocks<MODE>(PF
         else
           resample(std::false_type{});
       }
-      if (a.dbg_anc != nullptr) {
+      if (DBG && a.dbg_anc != nullptr) {
 #pragma unroll
         for (int i = 0; i < VPT; ++i)
           if (in_tile(i)) a.dbg_anc[(size_t)track * Kl + lbase + l0 + i] = anc[i];
@@ -1516,7 +1523,7 @@ __global__ void __launch_bounds__(PF_TILE / (VPT * R), fused_min_blocks<MODE>(PF
 #endif
       body(std::false_type{});
   }
-  if (a.dbg_anc != nullptr) {  // debug capture (parity tests): recompute-free copies
+  if (DBG && a.dbg_anc != nullptr) {  // debug capture (parity tests): recompute-free copies
 #pragma unroll
     for (int rr = 0; rr < R; ++rr) {
       const int l0 = (rr * TPB + tid) * VPT;
@@ -1525,7 +1532,7 @@ __global__ void __launch_bounds__(PF_TILE / (VPT * R), fused_min_blocks<MODE>(PF
         if (l0 + i < Tb) reinterpret_cast<real*>(a.dbg_L)[(size_t)track * Kl + lbase + l0 + i] = Lr[rr][i];
     }
   }
-  PF_TRACE(a, 4);
+  PF_TRACE_DBG(a, 4);
   // tile max (exact): warp max, one barrier, every thread reduces the NW values
 #pragma unroll
   for (int d = 16; d >= 1; d >>= 1) {
@@ -1696,7 +1703,7 @@ __global__ void __launch_bounds__(PF_TILE / (VPT * R), fused_min_blocks<MODE>(PF
       a.rec_Y[ri] = __double_as_longlong(by[0]);
     }
   }
-  PF_TRACE(a, 5);
+  PF_TRACE_DBG(a, 5);
   // complete only after the previous grid (keeps grid completion in stream
   // order: the next table reuses the exchange counters and records)
   if (a.t > 0 && tid == 0) pdl_wait();
