@@ -888,8 +888,12 @@ static int launch_frame(pf_handle* h, const void* map_slot, long long map_video_
   t.traj_stride = traj_stride;
   t.traj_index = traj_index;
   t.degenerate = h->d_degen;
-  const void* tk = h->km == 0 ? (const void*)pfk::pf_tile_table<0>
-                   : h->km == 1 ? (const void*)pfk::pf_tile_table<1> : (const void*)pfk::pf_tile_table<2>;
+  const void* tk = h->tracing ? (h->km == 0   ? (const void*)pfk::pf_tile_table<0, true>
+                                 : h->km == 1 ? (const void*)pfk::pf_tile_table<1, true>
+                                              : (const void*)pfk::pf_tile_table<2, true>)
+                              : (h->km == 0   ? (const void*)pfk::pf_tile_table<0>
+                                 : h->km == 1 ? (const void*)pfk::pf_tile_table<1>
+                                              : (const void*)pfk::pf_tile_table<2>);
   t.n_chunks = h->n_chunks;
   t.sync = h->tsync;
   t.agg = h->tagg;

@@ -1808,7 +1808,7 @@ __device__ __forceinline__ void scatter_windows_local(int2* wr, int n, long long
 // chunk subtrees are completed by the last CTA in tree order.  All CTAs of a
 // track are co-resident: each calls launch_dependents on entry, so the next
 // (dependent) grid cannot occupy the GPU before every table CTA has started.
-template <int MODE>
+template <int MODE, bool DBG = false>  // DBG: %globaltimer trace stamps (pf_set_trace)
 __global__ void __launch_bounds__(1024) pf_tile_table(TableArgs a) {
   __shared__ long long s_i[32];
   __shared__ double s_d[3 * 32 + 4];
@@ -1822,7 +1822,7 @@ __global__ void __launch_bounds__(1024) pf_tile_table(TableArgs a) {
   const bool valid = b < n;
   unsigned long long* sy = a.sync + (size_t)track * 4;
 
-  PF_TRACE(a, 0);
+  PF_TRACE_DBG(a, 0);
   pdl_launch_dependents();
   // the frame's resampling uniform: stream position t(2K+1)+2K
   const double u = pfr::uniform_of(a.ua * a.x0[track] + a.uc);
@@ -1830,7 +1830,7 @@ __global__ void __launch_bounds__(1024) pf_tile_table(TableArgs a) {
   const double Kd = __ll2double_rn(a.K);
   const double invK = __ddiv_rn(1.0, Kd);
   pdl_wait();  // tile records of this frame's fused kernel
-  PF_TRACE(a, 1);
+  PF_TRACE_DBG(a, 1);
   const size_t rb = (size_t)track * n + (valid ? b : 0);
   const double m1 = valid ? a.rec_m[rb] : __longlong_as_double(0xfff0000000000000LL);
   const long long S1 = valid ? a.rec_S[rb] : 0, X1 = valid ? a.rec_X[rb] : 0, Y1 = valid ? a.rec_Y[rb] : 0;
@@ -1838,7 +1838,7 @@ __global__ void __launch_bounds__(1024) pf_tile_table(TableArgs a) {
   // 1. global max (exact): the fused kernel's CTAs atomicMax'ed their tile
   //    maxima into sy[0] (order keys); reset by the last reader below
   const double m = okey_inv(__ldcg(sy + 0));
-  PF_TRACE(a, 4);
+  PF_TRACE_DBG(a, 4);
 
   // 2. exact fixed-point tile mass and its prefix across the chunk / track
   double f = 0.0;
@@ -1887,7 +1887,7 @@ __global__ void __launch_bounds__(1024) pf_tile_table(TableArgs a) {
     __syncthreads();
   }
   const double Sq = (double)Sqi;
-  PF_TRACE(a, 6);
+  PF_TRACE_DBG(a, 6);
 
   // 3. table entries and the estimate moments
   double vx = 0.0, vy = 0.0, vd = 0.0;
@@ -1923,7 +1923,7 @@ __global__ void __launch_bounds__(1024) pf_tile_table(TableArgs a) {
     vy = __dmul_rn(f, Y);
     vd = __dmul_rn(f, (double)S1);
   }
-  PF_TRACE(a, 7);
+  PF_TRACE_DBG(a, 7);
   // source windows of the next frame (scatter_windows)
   __syncthreads();
   if (valid) {
@@ -1956,7 +1956,7 @@ __global__ void __launch_bounds__(1024) pf_tile_table(TableArgs a) {
     __threadfence();
     atomicAdd(sy + 1, 1ULL);
   }
-  PF_TRACE(a, 5);
+  PF_TRACE_DBG(a, 5);
   // canonical pairwise tree: lanes, warps (zero padded), chunks (last CTA)
 #pragma unroll
   for (int d = 1; d < 32; d <<= 1) {
@@ -1993,7 +1993,7 @@ __global__ void __launch_bounds__(1024) pf_tile_table(TableArgs a) {
     }
   }
   __syncthreads();
-  PF_TRACE(a, 2);
+  PF_TRACE_DBG(a, 2);
   if (!s_last) return;
   if (nc > 1) {  // last CTA: tree over the chunk roots (power-of-two padded)
     __threadfence();
@@ -2053,7 +2053,7 @@ __global__ void __launch_bounds__(1024) pf_tile_table(TableArgs a) {
     double* tr = a.traj + ((size_t)track * a.traj_stride + a.traj_index) * 2;
     tr[0] = ex;
     tr[1] = ey;
-    PF_TRACE(a, 3);
+    PF_TRACE_DBG(a, 3);
     if (!(vd > 0.0) || !isfinite(vd) || !isfinite(ex) || !isfinite(ey)) atomicMin(a.degenerate + track, a.t);
     // every CTA of the track has passed the exchanges: reset them for the
     // next frame's table (which starts only after the next fused kernel
