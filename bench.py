@@ -246,6 +246,70 @@ def _config_block(cfg, args):
 # GPU arm
 # ---------------------------------------------------------------------------
 
+# ncu pipe names -> the microbenchmark kind that bounds them (pf_pipes.cu)
+PIPE_PEAK_OF = {"fp16": "hfma2", "fma": "ffma", "fp64": "dfma", "alu": "lop3", "lsu": "lds", "xu": "mufu_ex2"}
+
+
+def _ncu_profiles(config, prec):
+    """Per-launch counters of the committed ncu captures (profiles/ncu_pipes.json:
+    tools/pipes_capture.py; profiles/ncu_traffic.json: --set full)."""
+    out = {}
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as fh:
+            d = json.load(fh)
+        tr = d.get(f"{config}_{prec}") or d.get(f"{config}_{prec.split('-')[0]}")
+        if tr:
+            out["dram_bytes_per_launch"] = tr["dram_bytes_per_launch"]
+            out["source"] = "profiles/ncu_traffic.json (ncu --set full)"
+    except Exception:
+        pass
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_pipes.json")) as fh:
+            d = json.load(fh)
+        out["pipes"] = d["configs"][config][prec]
+    except Exception:
+        pass
+    return out
+
+
+def pipe_block(ncu, live_ms, device, clk):
+    """Per-pipe utilisation of the fused and map kernels: ncu per-launch
+    warp-instruction counts per pipe / live launch time, against the per-pipe
+    issue peaks measured on this box now (lib/libpf_pipes.so)."""
+    if "pipes" not in ncu:
+        return None
+    try:
+        import torch
+
+        from paper_2308_00763_b200.pipes import pipe_peaks
+
+        peaks = pipe_peaks(device)
+    except Exception as e:  # noqa: BLE001
+        return {"error": f"pipe microbenchmarks unavailable: {e}"}
+    sms = torch.cuda.get_device_properties(device).multi_processor_count
+    mhz = (clk or {}).get("sm_mhz") or 1965
+    out = {"peaks_warp_inst_per_sm_clk": peaks, "sm_mhz": mhz,
+           "source": "counts: profiles/ncu_pipes.json (ncu sm__inst_executed_pipe_*); peaks: measured now"}
+    for kern, ms in live_ms.items():
+        c = ncu["pipes"].get(kern)
+        if not c or not ms:
+            continue
+        if kern == "maps":
+            ms = ms / max(1, c.get("launches_per_step", 1))
+        cycles = ms * 1e-3 * mhz * 1e6 * sms  # SM-cycles of one launch
+        row = {"ms_per_launch": ms}
+        for pipe, pk in PIPE_PEAK_OF.items():
+            if pipe in c:
+                rate = c[pipe] / cycles
+                row[pipe] = {"warp_inst_per_launch": c[pipe], "per_sm_clk": rate, "peak": peaks[pk],
+                             "frac": rate / peaks[pk]}
+        if "total" in c:
+            row["issue"] = {"per_sm_clk": c["total"] / cycles, "peak": 4.0, "frac": c["total"] / cycles / 4.0,
+                            "peak_source": "4 schedulers x 1 warp-instruction per clock"}
+        out[kern] = row
+    return out
+
+
 
 def run_sharded(args, cfg, rank, world, local, dist, dev_frames, host_frames, truth, flush):
     """C5: one filter, particle range sharded over the ranks (strong scaling)."""
@@ -306,6 +370,19 @@ def run_sharded(args, cfg, rank, world, local, dist, dev_frames, host_frames, tr
 
 
 
+def relaunch(n: int) -> None:
+    import socket
+
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    rc = subprocess.call(cmd)
+    if rc:
+        raise SystemExit(rc)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -330,9 +407,16 @@ def main():
         cfg["tracks"] = args.tracks
     if args.particles:
         cfg["K"] = args.particles
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        # `python bench.py --gpus N` without a launcher: re-run this command
+        # under torchrun, one rank per GPU (127.0.0.1 rendezvous)
+        relaunch(args.gpus)
+        return
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world} (one rank per GPU)")
     if args.impl == "reference":
         run_reference_arm(args, cfg, rank, world)
         return
@@ -376,7 +460,7 @@ def main():
         return pf.Filter(K, precision, W, H, seeds=seeds, n_tracks=tracks, n_videos=nv, tpb=args.tpb,
                          device=local)
 
-    def device_steps(f, n, timed=True):
+    def device_steps(f, n, timed=True, parts=None):
         tot = 0.0
         launches = 0
         for _ in range(n):
@@ -384,8 +468,11 @@ def main():
             torch.cuda.synchronize()
             f.reset()
             f.run_frames(dev_frames, F)
-            tot += f.timings()["total"]
+            tm = f.timings()
+            tot += tm["total"]
             launches += f.launches()
+            if parts is not None:
+                parts.append(tm)
         return tot, launches
 
     def barrier():
@@ -410,7 +497,8 @@ def main():
     clocks = ClockSampler(local)
     barrier()
     clocks.start()
-    dev_ms, launches = device_steps(f, args.steps)
+    parts = []
+    dev_ms, launches = device_steps(f, args.steps, parts=parts)
     barrier()
     clk = clocks.stop()
     dev_ms = over_ranks(dev_ms)
@@ -440,6 +528,16 @@ def main():
            "ms_per_step": 1e3 * e2e_s / args.steps, "timer": "wall clock around pf_run (pinned host frames)"}
 
     # ---- roofline of the dominant kernel (fused frame kernel) ------------
+    # Timed inside the production schedule: the per-frame launch pair (fused
+    # kernel + its tile table, programmatic dependent launch, replayed from a
+    # CUDA graph) of the timed steps above -- device time of the frame region
+    # (CUDA events on the library stream around the graph) / F.  The pair
+    # overlaps under PDL, so this per-launch time is the frame period; the
+    # serialised per-kernel split (events between launches, no graph) gives
+    # the fused kernel's share of it.
+    frames_ms = statistics.mean(t["frames"] for t in parts)
+    maps_ms = statistics.mean(t["maps"] for t in parts)
+    period_ms = frames_ms / F
     f.set_profiling(True)
     flush.zero_()
     torch.cuda.synchronize()
@@ -448,39 +546,27 @@ def main():
     tm = f.timings()
     f.set_profiling(False)
     s = SIZES[prec]
-    fused_avg_ms = tm["frames"] / F
-    table_avg_ms = tm["tables"] / F
+    share = tm["frames"] / (tm["frames"] + tm["tables"])
     bytes_per_launch = tracks * K * 6 * s + nv * W * H
     peak, peak_src = _peaks()
-    achieved = bytes_per_launch / (fused_avg_ms * 1e-3) / 1e9
-    traffic = None
-    warp_inst = None
-    try:
-        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as fh:
-            d = json.load(fh)
-            tr = d.get(f"{args.config}_{prec}") or d.get(f"{args.config}_{prec.split('-')[0]}")
-            if tr:
-                traffic = tr["dram_bytes_per_launch"]
-                warp_inst = tr.get("warp_inst_per_launch")
-    except Exception:
-        pass
+    achieved = bytes_per_launch / (period_ms * 1e-3) / 1e9
+    ncu = _ncu_profiles(args.config, prec)
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                "traffic": traffic, "kernel": f"pf_fused_frame<{prec}>",
-                "algorithmic_bytes_per_launch": bytes_per_launch,
-                "bytes_per_particle": 6 * s, "avg_launch_ms": fused_avg_ms, "tile_table_avg_ms": table_avg_ms,
-                "maps_ms_per_step": tm["maps"], "peak_source": peak_src}
-    if warp_inst:
-        # the bound that binds: instruction issue, 4 warp-instructions
-        # per clock per SM; instruction count from the committed ncu capture
-        import torch
-
-        sms = torch.cuda.get_device_properties(local).multi_processor_count
-        mhz = (clk or {}).get("sm_mhz") or 1965
-        peak_issue = sms * 4 * mhz * 1e6
-        ach_issue = warp_inst / (fused_avg_ms * 1e-3)
-        roofline["issue"] = {"achieved": ach_issue, "peak": peak_issue, "unit": "warp-inst/s",
-                             "frac": ach_issue / peak_issue, "warp_inst_per_launch": warp_inst,
-                             "source": "ncu Executed Instructions (profiles/ncu_traffic.json), live launch time"}
+                "traffic": ncu.get("dram_bytes_per_launch"), "kernel": f"pf_fused_frame<{prec}>",
+                "algorithmic_bytes_per_launch": bytes_per_launch, "bytes_per_particle": 6 * s,
+                "avg_launch_ms": period_ms,
+                "timing": ("in the production schedule: frame-region device time of the timed steps / F "
+                           "(fused + tile table per frame, PDL-overlapped, CUDA graph)"),
+                "frames_x_launch_ms": frames_ms, "ms_per_step": dev_ms / args.steps,
+                "serialised": {"fused_ms": tm["frames"] / F, "tile_table_ms": tm["tables"] / F,
+                               "fused_share": share,
+                               "how": "events between launches, no graph, no PDL overlap (one extra step)"},
+                "maps_ms_per_step": maps_ms, "peak_source": peak_src,
+                "traffic_source": ncu.get("source")}
+    assert frames_ms <= dev_ms / args.steps * (1 + 1e-6), (frames_ms, dev_ms / args.steps)
+    pipes_line = pipe_block(ncu, {"fused": period_ms, "maps": maps_ms}, local, clk)
+    if pipes_line:
+        roofline["pipes"] = pipes_line
     f.close()
 
     # ---- the other precisions of the same workload -----------------------
@@ -489,18 +575,49 @@ def main():
         for p2 in ("fp16", "fp32", "fp64"):
             g = make(p2)
             device_steps(g, 2)
-            ms2, _ = device_steps(g, max(3, args.steps // 2))
+            parts2 = []
+            ms2, _ = device_steps(g, max(3, args.steps // 2), parts=parts2)
             ms2 = over_ranks(ms2)
             v2 = updates_per_step * max(3, args.steps // 2) / (ms2 * 1e-3)
             g.reset()
             t2 = g.run_frames(dev_frames, F)
             e2 = pf.accuracy_metrics(t2[0], truth)
-            extra[p2] = {"value": v2, "unit": UNIT, "tracking_rmse_px": e2[0], "tracking_mean_err_px": e2[1]}
+            per2 = statistics.mean(t["frames"] for t in parts2) / F
+            b2 = tracks * K * 6 * SIZES[p2] + nv * W * H
+            extra[p2] = {"value": v2, "unit": UNIT, "tracking_rmse_px": e2[0], "tracking_mean_err_px": e2[1],
+                         "frame_period_ms": per2, "hbm_frac": b2 / (per2 * 1e-3) / 1e9 / peak}
+            pl = pipe_block(_ncu_profiles(args.config, p2),
+                            {"fused": per2, "maps": statistics.mean(t["maps"] for t in parts2)}, local, clk)
+            if pl:
+                extra[p2]["pipes"] = pl
             g.close()
-        extra[prec] = {"value": value, "unit": UNIT, "tracking_rmse_px": rmse, "tracking_mean_err_px": mean_err}
+        extra[prec] = {"value": value, "unit": UNIT, "tracking_rmse_px": rmse, "tracking_mean_err_px": mean_err,
+                       "frame_period_ms": period_ms, "hbm_frac": achieved / peak}
         extra["fp16_over_fp32"] = value / extra["fp32"]["value"]
         extra["fp16_over_fp64"] = value / extra["fp64"]["value"]
         extra["packed_over_scalar_fp16"] = value / extra["fp16"]["value"]
+
+    # ---- per-frame API latency: Filter.step (the reference's per-frame run
+    # and estimate, filter.py:617-654) on host frames and on device frames
+    step_lat = None
+    if not args.no_extra and tracks == 1:
+        g = make(prec)
+        host1 = np.ascontiguousarray(host_frames[:F] if nv == 1 else host_frames[0])
+        lat = {}
+        for label, src in (("host_frame", host1), ("device_frame", dev_frames if nv == 1 else dev_frames[0])):
+            g.reset()
+            for t in range(5):
+                g.step(src[t])
+            g.reset()
+            n_lat = min(F, 50)
+            t0 = time.perf_counter()
+            for t in range(n_lat):
+                g.step(src[t])
+            lat[label] = {"us_per_frame": 1e6 * (time.perf_counter() - t0) / n_lat, "frames": n_lat}
+        g.close()
+        step_lat = dict(lat, api="Filter.step(frame) -> (x, y): frame in, likelihood map, fused frame kernel, "
+                                 "tile table, estimate D2H, host sync -- wall clock per call",
+                        particles=K, precision=prec)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -525,6 +642,7 @@ def main():
             "gpu_launches": launches,
             "tracking": {"rmse_px": rmse, "mean_err_px": mean_err, "max_err_px": max_err},
             "by_precision": extra or None,
+            "step_latency": step_lat,
         }
         print(json.dumps(line), flush=True)
     if dist is not None:

@@ -90,6 +90,20 @@ int pf_run(pf_handle* h, const uint8_t* frames, int32_t n_frames, int32_t frames
 /* One frame for every track: frame: [n_videos][H][W] u8; est_out host [n_tracks][2]. */
 int pf_step(pf_handle* h, const uint8_t* frame, int32_t frame_on_device, double* est_out);
 
+/* Stream-ordered variants (no host synchronisation).  `stream` is a
+ * cudaStream_t of the handle's device (NULL = none): the run starts after the
+ * work already queued on `stream` (e.g. the kernels producing device frames),
+ * and work queued on `stream` afterwards sees traj_out / est_out, which may be
+ * device, pinned host or pageable host memory (a pageable destination makes
+ * the final copy blocking).  Frame buffers must stay valid until the run has
+ * completed.  pf_sync waits for the handle's enqueued run and returns
+ * PF_EDEGENERATE / timings exactly as pf_run would.  This is the stream-ordered
+ * form of the frame loop of run() (filter.py:617-654). */
+int pf_run_async(pf_handle* h, const uint8_t* frames, int32_t n_frames, int32_t frames_on_device, double* traj_out,
+                 void* stream);
+int pf_step_async(pf_handle* h, const uint8_t* frame, int32_t frame_on_device, double* est_out, void* stream);
+int pf_sync(pf_handle* h);
+
 int pf_degenerate_frame(const pf_handle* h);
 
 /* Debug/parity: the per-frame likelihood maps of F host frames (one video),
@@ -188,6 +202,26 @@ int64_t pf_last_launches(const pf_handle* h);
 /* Debug/parity: copy track `track` state to host.  xs, ys, cdf_local in the
  * mode dtype (fp16 as uint16 bit patterns); any pointer may be NULL. */
 int pf_get_state(pf_handle* h, int32_t track, void* xs, void* ys, void* cdf_local);
+/* Draw stream of the fused path: switch the handle (one unsharded track,
+ * 128 or 256 threads per block) from the product LCG stream to the
+ * reference's own stream, Generator(Philox(seed)) (filter.py:71-82, RngStream):
+ * frame t consumes standard_normal((K, 2)) then random(), exactly as run()
+ * does (filter.py:617-650), generated in parallel on the device
+ * (pf_philox.cuh).  state11 = NumPy's Philox state after seeding: key[2],
+ * counter[4], buffer[4], buffer_pos (np.random.Philox(seed).state).  pf_reset
+ * rewinds the stream to this state; pf_set_state leaves it where it is.
+ * Debug capture (pf_get_debug) and tracing are not available in this mode. */
+int pf_set_rng_philox(pf_handle* h, const uint64_t* state11);
+
+/* State injection (teacher forcing / snapshot restore): track `track`'s
+ * positions become xs, ys (mode dtype, fp16 as uint16 patterns) as the
+ * post-resample state entering frame `frame`.  The next frame of EVERY track
+ * then runs with identity ancestors (the positions are already resampled)
+ * and frame `frame`'s draws; the frames after it proceed normally.  The
+ * reference's seam for the same thing is a stage_hook mutating ParticleSet
+ * after "resample" (filter.py:617-654; pkg/tests/test_filter.py:391-393).
+ * Not available on sharded handles. */
+int pf_set_state(pf_handle* h, int32_t track, const void* xs, const void* ys, int64_t frame);
 /* Last frame's ancestors (int64 [K]) and per-particle log-likelihoods (mode dtype). */
 int pf_get_debug(pf_handle* h, int32_t track, int64_t* ancestors, void* loglik);
 
@@ -220,14 +254,17 @@ int pf_rng_normals(uint64_t seed, uint64_t pos, int64_t n, double* out, int32_t 
 int pf_rng_uniforms(uint64_t seed, uint64_t pos, int64_t n, double* out, int32_t device);
 
 /* NumPy-compatible reference stream (Generator(Philox(seed)), filter.py:71-82)
- * generated on the device for the staged parity engine.  state11 = NumPy's
- * Philox state: key[2], counter[4], buffer[4], buffer_pos.  Draws are
- * sequential (variable ziggurat consumption): one device thread per stream. */
+ * generated on the device.  state11 = NumPy's Philox state: key[2],
+ * counter[4], buffer[4], buffer_pos.  The ziggurat's variable word
+ * consumption is resolved in parallel (pf_philox.cuh: classify every word
+ * position, speculate block entries, repair, scan, emit). */
 typedef struct pf_philox pf_philox;
 int pf_philox_create(pf_philox** out, const uint64_t* state11, int32_t device);
 int pf_philox_destroy(pf_philox* p);
 int pf_philox_normals(pf_philox* p, int64_t n, double* out);
 int pf_philox_uniforms(pf_philox* p, int64_t n, double* out);
+/* the same normals into device memory, stream-ordered on `stream` (no sync) */
+int pf_philox_normals_device(pf_philox* p, int64_t n, double* out_dev, void* stream);
 
 /* RN16(exp(x)) for all 65536 binary16 patterns (host-built table used by the
  * kernels; exposed so tests can pin it against halfnum.exp16 on CPU). */

@@ -118,11 +118,20 @@ class FusedTrack:
         self.table = None  # (s, O, invM)
         self.u = None
         self.t = 0
+        self.ident = False  # next frame: identity ancestors (injected state)
+
+    def set_state(self, xs: np.ndarray, ys: np.ndarray, t: int) -> None:
+        """pf_set_state: post-resample positions entering frame t."""
+        with np.errstate(over="ignore"):
+            self.xs = np.asarray(xs).astype(self.d)
+            self.ys = np.asarray(ys).astype(self.d)
+        self.t = int(t)
+        self.ident = True
 
     # -- stages ------------------------------------------------------------
     def ancestors(self) -> np.ndarray:
         K = self.K
-        if self.t == 0:
+        if self.t == 0 or self.ident:
             return np.arange(K, dtype=np.int64)
         s, O, invM = self.table
         k = np.arange(K, dtype=np.int64)
@@ -138,12 +147,14 @@ class FusedTrack:
             q = np.minimum(np.maximum(q, 0.0), 1.0)
         anc = np.empty(K, dtype=np.int64)
         c64 = self.c.astype(np.float64)
-        for tb in np.unique(b):
-            sel = b == tb
+        # b is non-decreasing in k: each source tile's outputs are one contiguous run
+        tiles = np.unique(b)
+        starts = np.searchsorted(b, tiles, side="left")
+        ends = np.searchsorted(b, tiles, side="right")
+        for tb, k0, k1 in zip(tiles.tolist(), starts.tolist(), ends.tolist()):
             lo = tb * TILE
             hi = min(K, lo + TILE)
-            j = np.searchsorted(c64[lo:hi], q[sel], side="left")
-            anc[sel] = lo + j
+            anc[k0:k1] = lo + np.searchsorted(c64[lo:hi], q[k0:k1], side="left")
         return anc
 
     def propagate(self, anc: np.ndarray, noise: np.ndarray):
@@ -245,12 +256,16 @@ class FusedTrack:
             self.table = (s, O, invM)
         return ex, ey
 
-    def step(self, Lmap: np.ndarray) -> Tuple[float, float]:
+    def step(self, Lmap: np.ndarray, noise: Optional[np.ndarray] = None, u: Optional[float] = None
+             ) -> Tuple[float, float]:
+        """One frame; draws from the LCG stream unless given (noise (K, 2), u),
+        e.g. the reference's Generator(Philox(seed)) stream (rng='numpy-philox')."""
         K = self.K
-        base = self.t * (2 * K + 1)
-        words = rng.lcg_words(self.x0, base, 2 * K)
-        noise = rng.normals_from_lcg_words(words).reshape(K, 2)
-        u = (rng.lcg_word(self.x0, base + 2 * K) >> 11) * rng.TWO_M53
+        if noise is None:
+            base = self.t * (2 * K + 1)
+            words = rng.lcg_words(self.x0, base, 2 * K)
+            noise = rng.normals_from_lcg_words(words).reshape(K, 2)
+            u = (rng.lcg_word(self.x0, base + 2 * K) >> 11) * rng.TWO_M53
         anc = self.ancestors()
         self.last_ancestors = anc
         self.propagate(anc, noise)
@@ -260,6 +275,7 @@ class FusedTrack:
         est = self.table_step(m_b, S, X, Y, u)
         self.u = u
         self.t += 1
+        self.ident = False
         return est
 
     def loglik_map(self, frame: np.ndarray) -> np.ndarray:

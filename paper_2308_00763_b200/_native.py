@@ -62,6 +62,9 @@ SIGNATURES = [
     ("pf_reset", C.c_int, [_VP, C.c_double, C.c_double]),
     ("pf_run", C.c_int, [_VP, _VP, C.c_int32, C.c_int32, _VP]),
     ("pf_step", C.c_int, [_VP, _VP, C.c_int32, _VP]),
+    ("pf_run_async", C.c_int, [_VP, _VP, C.c_int32, C.c_int32, _VP, _VP]),
+    ("pf_step_async", C.c_int, [_VP, _VP, C.c_int32, _VP, _VP]),
+    ("pf_sync", C.c_int, [_VP]),
     ("pf_degenerate_frame", C.c_int, [_VP]),
     ("pf_likelihood_maps", C.c_int, [_VP, _VP, C.c_int32, _VP]),
     ("pf_set_profiling", C.c_int, [_VP, C.c_int32]),
@@ -88,6 +91,8 @@ SIGNATURES = [
     ("pf_shard_local_allgather", C.c_int, [_VP, C.c_int32, C.c_int32]),
     ("pf_get_trace", C.c_int, [_VP, _VP, C.c_int64]),
     ("pf_get_state", C.c_int, [_VP, C.c_int32, _VP, _VP, _VP]),
+    ("pf_set_rng_philox", C.c_int, [_VP, _VP]),
+    ("pf_set_state", C.c_int, [_VP, C.c_int32, _VP, _VP, C.c_int64]),
     ("pf_get_debug", C.c_int, [_VP, C.c_int32, _VP, _VP]),
     ("pf_stage_create", C.c_int, [C.POINTER(_VP), C.c_int32, C.c_int64, C.POINTER(pf_params), _VP, C.c_int32, C.c_int32]),
     ("pf_stage_destroy", C.c_int, [_VP]),
@@ -111,6 +116,7 @@ SIGNATURES = [
     ("pf_philox_destroy", C.c_int, [_VP]),
     ("pf_philox_normals", C.c_int, [_VP, C.c_int64, _VP]),
     ("pf_philox_uniforms", C.c_int, [_VP, C.c_int64, _VP]),
+    ("pf_philox_normals_device", C.c_int, [_VP, C.c_int64, _VP, _VP]),
 ]
 
 _lib = None

@@ -19,6 +19,7 @@
 
 #include "../../include/pf_b200.h"
 #include "pf_kernels.cuh"
+#include "pf_philox.cuh"
 #include "pf_staged.cuh"
 #include "pf_video.cuh"
 // host copies of the ziggurat tables
@@ -135,6 +136,110 @@ int next_pow2(long long v) {
 
 }  // namespace
 
+// Parallel generator of the reference's Philox stream (pf_philox.cuh): scratch
+// sized for the largest draw seen, the stream state and its device position.
+struct PhxGen {
+  pfp::PhxStream s{};
+  unsigned long long* P = nullptr;  // device word position
+  int* status = nullptr;            // device: nonzero if a window ran short
+  double* v = nullptr;
+  int *L = nullptr, *exit0 = nullptr, *entry = nullptr, *count = nullptr, *exitb = nullptr, *bad = nullptr;
+  long long* base = nullptr;
+  double* u_scratch = nullptr;
+  int cap_blk = 0;
+
+  void release() {
+    void* ps[] = {P, status, v, L, exit0, entry, count, exitb, bad, base, u_scratch};
+    for (void* q : ps)
+      if (q) cudaFree(q);
+    *this = PhxGen{};
+  }
+  // state11 = NumPy Philox state: key[2], counter[4], buffer[4], buffer_pos
+  int init(const uint64_t* state11, std::string& err) {
+    s.key[0] = state11[0];
+    s.key[1] = state11[1];
+    for (int i = 0; i < 4; ++i) s.ctr[i] = state11[2 + i];
+    for (int i = 0; i < 4; ++i) s.buf[i] = state11[6 + i];
+    s.pos = (int)state11[10];
+    if (s.pos < 0 || s.pos > 4) {
+      err = "bad Philox buffer position";
+      return PF_EINVAL;
+    }
+    if (!P) {
+      PF_CUDA(cudaMalloc(&P, 8), err);
+      PF_CUDA(cudaMalloc(&status, 4), err);
+      PF_CUDA(cudaMalloc(&u_scratch, 8), err);
+    }
+    return rewind(nullptr, err);
+  }
+  int rewind(cudaStream_t st, std::string& err) {
+    PF_CUDA(cudaMemsetAsync(P, 0, 8, st), err);
+    PF_CUDA(cudaMemsetAsync(status, 0, 4, st), err);
+    return PF_OK;
+  }
+  int reserve(long long n, std::string& err) {
+    const int nb = pfp::window_blocks(n);
+    if (nb <= cap_blk) return PF_OK;
+    void* ps[] = {v, L, exit0, entry, count, exitb, bad, base};
+    for (void* q : ps)
+      if (q) cudaFree(q);
+    const size_t W = (size_t)nb * pfp::kBlk;
+    PF_CUDA(cudaMalloc(&v, W * 8), err);
+    PF_CUDA(cudaMalloc(&L, W * 4), err);
+    PF_CUDA(cudaMalloc(&exit0, nb * 4), err);
+    PF_CUDA(cudaMalloc(&entry, nb * 4), err);
+    PF_CUDA(cudaMalloc(&count, nb * 4), err);
+    PF_CUDA(cudaMalloc(&exitb, nb * 4), err);
+    PF_CUDA(cudaMalloc(&bad, nb * 4), err);
+    PF_CUDA(cudaMalloc(&base, nb * 8), err);
+    cap_blk = nb;
+    return PF_OK;
+  }
+  // n normals into out (device) and, with u_out, the random() after them
+  int draw(cudaStream_t st, long long n, double* out, double* u_out, std::string& err) {
+    int rc = reserve(n, err);
+    if (rc) return rc;
+    pfp::GenArgs a{};
+    a.s = s;
+    a.P = P;
+    a.n = n;
+    a.nblk = pfp::window_blocks(n);
+    a.v = v;
+    a.L = L;
+    a.exit0 = exit0;
+    a.entry = entry;
+    a.count = count;
+    a.exitb = exitb;
+    a.bad = bad;
+    a.base = base;
+    a.out = out;
+    a.u_out = u_out ? u_out : u_scratch;
+    a.status = status;
+    a.take_uniform = u_out ? 1 : 0;
+    pfp::phx_classify<<<a.nblk, pfp::kThreads, 0, st>>>(a);
+    pfp::phx_resolve<<<a.nblk, pfp::kThreads, 0, st>>>(a);
+    pfp::phx_scan<<<1, pfp::kThreads, 0, st>>>(a);
+    pfp::phx_emit<<<a.nblk, pfp::kThreads, 0, st>>>(a);
+    PF_CUDA(cudaGetLastError(), err);
+    return PF_OK;
+  }
+  int uniforms(cudaStream_t st, long long m, double* out, std::string& err) {
+    pfp::phx_uniforms<<<(unsigned)((m + 255) / 256), 256, 0, st>>>(s, P, m, out);
+    pfp::phx_advance<<<1, 1, 0, st>>>(P, m);
+    PF_CUDA(cudaGetLastError(), err);
+    return PF_OK;
+  }
+  int check(std::string& err) {  // after a synchronisation
+    int h = 0;
+    PF_CUDA(cudaMemcpy(&h, status, 4, cudaMemcpyDeviceToHost), err);
+    if (h) {
+      err = "Philox stream: draw window too small (internal error)";
+      return PF_ECUDA;
+    }
+    return PF_OK;
+  }
+};
+
 // host frames are uploaded in this many chunks on a copy stream; each
 // chunk's likelihood maps start as soon as it lands (pf_run)
 constexpr int kUploadChunks = 8;
@@ -227,6 +332,23 @@ struct pf_handle {
   unsigned long long* d_trace = nullptr;  // pf_set_trace: [frame][n_tiles + n_chunks][8]
   size_t trace_cap = 0;
   bool tracing = false;
+  // stream-ordered calls (pf_run_async): caller-stream handoff events, and
+  // whether a run is enqueued but not yet completed (pf_sync)
+  cudaEvent_t xin = nullptr, xout = nullptr;
+  bool pending = false;
+  int pending_F = 0;
+  // pf_set_state: the next frame runs with identity ancestors (injected state)
+  bool ident_next = false;
+  bool g_ident = false;
+  // rng = numpy-philox (pf_set_rng_philox): every frame's 2K normals and
+  // uniform come from the reference's own stream, generated before the frames
+  bool philox = false;
+  PhxGen phx;
+  double* noise_all = nullptr;  // [F][K][2]
+  size_t noise_cap = 0;
+  double* u_all = nullptr;  // [F]
+  size_t u_cap = 0;
+  const void* g_noise = nullptr;
 };
 
 typedef void (*fused_fn)(pfk::FusedArgs);
@@ -247,6 +369,12 @@ template <int M>
 static fused_fn fused_sharded(int tpb) {
   return tpb == 128 ? pfk::pf_fused_frame<M, 8, 1, true> : pfk::pf_fused_frame<M, 4, 1, true>;
 }
+// numpy-philox stream: normals read from the generated buffer (128 / 256 threads)
+template <int M, bool PK>
+static fused_fn fused_nz(int tpb) {
+  return tpb == 128 ? pfk::pf_fused_frame<M, 8, 1, false, PK, false, true>
+                    : pfk::pf_fused_frame<M, 4, 1, false, PK, false, true>;
+}
 // dbg: the instantiation with the trace / debug-capture hooks (pf_set_trace,
 // pf_get_debug); the production kernels carry neither
 template <bool DBG>
@@ -259,13 +387,17 @@ static bool fused_dbg(const pf_handle* h) { return h->n_shards == 1 && (h->dbg_a
 static fused_fn fused_kernel(const pf_handle* h, int dbg = -1) {
   if (h->n_shards > 1)
     return h->km == 0 ? fused_sharded<0>(h->tpb) : h->km == 1 ? fused_sharded<1>(h->tpb) : fused_sharded<2>(h->tpb);
+  if (h->philox) {
+    if (h->km == 2) return h->precision == PF_FP16 ? fused_nz<2, false>(h->tpb) : fused_nz<2, true>(h->tpb);
+    return h->km == 0 ? fused_nz<0, true>(h->tpb) : fused_nz<1, true>(h->tpb);
+  }
   const bool d = dbg < 0 ? fused_dbg(h) : dbg != 0;
   return d ? fused_unsharded<true>(h) : fused_unsharded<false>(h);
 }
 static cudaError_t set_fused_smem(const pf_handle* h) {
   cudaError_t e = cudaFuncSetAttribute((const void*)fused_kernel(h, 0), cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)h->fused_smem);
-  if (e == cudaSuccess && h->n_shards == 1)
+  if (e == cudaSuccess && h->n_shards == 1 && !h->philox)
     e = cudaFuncSetAttribute((const void*)fused_kernel(h, 1), cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)h->fused_smem);
   return e;
@@ -345,7 +477,13 @@ int pf_destroy(pf_handle* h) {
     if (h->peer_ipc[sh])
       for (int i = 0; i < 8; ++i)
         if (h->peer[sh][i]) cudaIpcCloseMemHandle(h->peer[sh][i]);
+  if (h->pending) cudaStreamSynchronize(h->stream);
+  h->phx.release();
+  if (h->noise_all) cudaFree(h->noise_all);
+  if (h->u_all) cudaFree(h->u_all);
   if (h->xev) cudaEventDestroy(h->xev);
+  if (h->xin) cudaEventDestroy(h->xin);
+  if (h->xout) cudaEventDestroy(h->xout);
   if (h->h_degen) cudaFreeHost(h->h_degen);
   for (auto& e : h->ev)
     if (e) cudaEventDestroy(e);
@@ -708,6 +846,7 @@ int pf_reset(pf_handle* h, double x0, double y0) {
   h->start_y = y0;
   h->cur = 0;
   h->frame_counter = 0;
+  h->ident_next = false;
   h->degenerate_frame = -1;
   const long long n = h->Kl * h->n_tracks;
   const int tb = 256;
@@ -723,6 +862,10 @@ int pf_reset(pf_handle* h, double x0, double y0) {
   PF_CUDA(cudaMemcpyAsync(h->d_degen, dg.data(), h->n_tracks * sizeof(int), cudaMemcpyHostToDevice, h->stream),
           h->err);
   PF_CUDA(cudaMemsetAsync(h->tsync, 0, (size_t)h->n_tracks * 4 * 8, h->stream), h->err);
+  if (h->philox) {  // the reference stream restarts from its seeded state
+    const int rc = h->phx.rewind(h->stream, h->err);
+    if (rc) return rc;
+  }
   PF_CUDA(cudaStreamSynchronize(h->stream), h->err);
   return PF_OK;
 }
@@ -817,6 +960,8 @@ static int launch_frame(pf_handle* h, const void* map_slot, long long map_video_
   a.r = h->r;
   a.Wm = h->Wm;
   a.t = (int)h->frame_counter;
+  a.ident = (h->frame_counter == 0 || h->ident_next) ? 1 : 0;
+  h->ident_next = false;
   a.X_new = h->X[1 - h->cur];
   a.C_new = h->C[1 - h->cur];
   a.u_prev = h->u;
@@ -848,6 +993,7 @@ static int launch_frame(pf_handle* h, const void* map_slot, long long map_video_
   a.ready_target = ordered ? 0ULL : (unsigned long long)h->n_chunks * (unsigned long long)h->frame_counter;
   const size_t tr_frame = (size_t)(h->n_tiles + h->n_chunks) * 8;
   a.trace = (h->tracing && h->d_trace) ? h->d_trace + (size_t)traj_index * tr_frame : nullptr;
+  a.noise = h->philox ? reinterpret_cast<const double2*>(h->noise_all + (size_t)traj_index * 2 * h->K) : nullptr;
   PF_CUDA(launch_pdl(h, (const void*)fused_kernel(h), dim3(h->nl, h->n_tracks), dim3(h->tpb), h->fused_smem, a,
                      !ordered),
           h->err);
@@ -899,6 +1045,7 @@ static int launch_frame(pf_handle* h, const void* map_slot, long long map_video_
   t.agg = h->tagg;
   t.roots = h->troots;
   t.win = h->win;
+  t.u_in = h->philox ? h->u_all + traj_index : nullptr;
   t.trace = (h->tracing && h->d_trace) ? h->d_trace + (size_t)traj_index * tr_frame + (size_t)h->n_tiles * 8 : nullptr;
   PF_CUDA(launch_pdl(h, tk, dim3(h->n_chunks, h->n_tracks), dim3(h->tpb_table), 0, t), h->err);
   PF_CUDA(cudaGetLastError(), h->err);
@@ -930,13 +1077,25 @@ static int finish_degenerate(pf_handle* h) {  // after the stream is synchronise
   return PF_OK;
 }
 
-int pf_run(pf_handle* h, const uint8_t* frames, int32_t F, int32_t on_device, double* traj_out) {
+// Enqueue a whole-video run on the handle's stream, ordered after `ext`'s
+// prior work when ext is given (and `ext` ordered after the run); no host
+// synchronisation.  run_complete() waits and reads the timings / degeneracy.
+static int run_enqueue(pf_handle* h, const uint8_t* frames, int32_t F, int32_t on_device, double* traj_out,
+                       cudaStream_t ext) {
   if (!h || !frames || F < 1 || !traj_out) return PF_EINVAL;
   if (h->n_shards > 1) {
     h->err = "sharded handle: drive frames with pf_shard_*";
     return PF_EINVAL;
   }
   PF_CUDA(cudaSetDevice(h->device), h->err);
+  if (ext) {
+    if (!h->xin) {
+      PF_CUDA(cudaEventCreateWithFlags(&h->xin, cudaEventDisableTiming), h->err);
+      PF_CUDA(cudaEventCreateWithFlags(&h->xout, cudaEventDisableTiming), h->err);
+    }
+    PF_CUDA(cudaEventRecord(h->xin, ext), h->err);  // the caller's producers of `frames`
+    PF_CUDA(cudaStreamWaitEvent(h->stream, h->xin, 0), h->err);
+  }
   h->launches = 0;
   const size_t fbytes = (size_t)h->n_videos * F * h->H * h->W;
   const size_t map_elems = (size_t)h->Hm * h->Wm;
@@ -992,18 +1151,29 @@ int pf_run(pf_handle* h, const uint8_t* frames, int32_t F, int32_t on_device, do
     PF_CUDA(cudaEventRecord(h->ev[1], h->stream), h->err);
     if ((rc = launch_maps(h, dframes, F))) return rc;
   }
+  if (h->philox) {  // the reference stream's draws of every frame: 2K normals, then random()
+    if ((rc = grow((void**)&h->noise_all, &h->noise_cap, (size_t)F * 2 * h->K * 8, h->err))) return rc;
+    if ((rc = grow((void**)&h->u_all, &h->u_cap, (size_t)F * 8, h->err))) return rc;
+    for (int f = 0; f < F; ++f)
+      if ((rc = h->phx.draw(h->stream, 2 * h->K, h->noise_all + (size_t)f * 2 * h->K, h->u_all + f, h->err)))
+        return rc;
+    h->launches += 4LL * F;
+  }
   PF_CUDA(cudaEventRecord(h->ev[2], h->stream), h->err);
   const long long vstride = (long long)F * map_elems;  // elements between videos
   const bool graph_ok = h->use_graphs && !h->profiling && F >= 4;
   if (graph_ok && h->gexec && h->g_start == h->frame_counter && h->g_cur == h->cur && h->g_F == F &&
-      h->g_maps == h->d_maps && h->g_traj == h->d_traj) {
+      h->g_maps == h->d_maps && h->g_traj == h->d_traj && h->g_ident == h->ident_next &&
+      h->g_noise == (const void*)h->noise_all) {
     PF_CUDA(cudaGraphLaunch(h->gexec, h->stream), h->err);
+    h->ident_next = false;
     h->frame_counter += F;
     if (F % 2) h->cur = 1 - h->cur;
     h->launches += 2LL * F;
   } else if (graph_ok) {
     const long long start = h->frame_counter;
     const int cur0 = h->cur;
+    const bool ident0 = h->ident_next;
     cudaGraph_t g = nullptr;
     PF_CUDA(cudaStreamBeginCapture(h->stream, cudaStreamCaptureModeThreadLocal), h->err);
     for (int f = 0; f < F; ++f) {
@@ -1021,6 +1191,8 @@ int pf_run(pf_handle* h, const uint8_t* frames, int32_t F, int32_t on_device, do
     cudaGraphDestroy(g);
     h->g_start = start;
     h->g_cur = cur0;
+    h->g_ident = ident0;
+    h->g_noise = h->noise_all;
     h->g_F = F;
     h->g_maps = h->d_maps;
     h->g_traj = h->d_traj;
@@ -1032,11 +1204,31 @@ int pf_run(pf_handle* h, const uint8_t* frames, int32_t F, int32_t on_device, do
     }
   }
   PF_CUDA(cudaEventRecord(h->ev[3], h->stream), h->err);
-  PF_CUDA(cudaMemcpyAsync(traj_out, h->d_traj, (size_t)h->n_tracks * F * 2 * 8, cudaMemcpyDeviceToHost, h->stream),
+  // device or (pinned / pageable) host destination
+  PF_CUDA(cudaMemcpyAsync(traj_out, h->d_traj, (size_t)h->n_tracks * F * 2 * 8, cudaMemcpyDefault, h->stream),
           h->err);
   if ((rc = queue_degenerate(h))) return rc;
   PF_CUDA(cudaEventRecord(h->ev[4], h->stream), h->err);
+  if (ext) {  // the caller's later work sees the trajectory
+    PF_CUDA(cudaEventRecord(h->xout, h->stream), h->err);
+    PF_CUDA(cudaStreamWaitEvent(ext, h->xout, 0), h->err);
+  }
+  h->pending = true;
+  h->pending_F = F;
+  return PF_OK;
+}
+
+// wait for the enqueued run; timings and the degeneracy check
+static int run_complete(pf_handle* h) {
+  if (!h->pending) return PF_OK;
+  PF_CUDA(cudaSetDevice(h->device), h->err);
   PF_CUDA(cudaStreamSynchronize(h->stream), h->err);
+  h->pending = false;
+  const int F = h->pending_F;
+  if (h->philox) {
+    const int rc = h->phx.check(h->err);
+    if (rc) return rc;
+  }
   float ms;
   cudaEventElapsedTime(&ms, h->ev[0], h->ev[4]);
   h->timings[0] = ms;
@@ -1061,6 +1253,26 @@ int pf_run(pf_handle* h, const uint8_t* frames, int32_t F, int32_t on_device, do
   cudaEventElapsedTime(&ms, h->ev[3], h->ev[4]);
   h->timings[5] = ms;
   return finish_degenerate(h);
+}
+
+int pf_run(pf_handle* h, const uint8_t* frames, int32_t F, int32_t on_device, double* traj_out) {
+  int rc = run_enqueue(h, frames, F, on_device, traj_out, nullptr);
+  if (rc) return rc;
+  return run_complete(h);
+}
+
+int pf_run_async(pf_handle* h, const uint8_t* frames, int32_t F, int32_t on_device, double* traj_out,
+                 void* stream) {
+  return run_enqueue(h, frames, F, on_device, traj_out, (cudaStream_t)stream);
+}
+
+int pf_step_async(pf_handle* h, const uint8_t* frame, int32_t on_device, double* est_out, void* stream) {
+  return run_enqueue(h, frame, 1, on_device, est_out, (cudaStream_t)stream);
+}
+
+int pf_sync(pf_handle* h) {
+  if (!h) return PF_EINVAL;
+  return run_complete(h);
 }
 
 int pf_likelihood_maps(pf_handle* h, const uint8_t* frames, int32_t F, void* maps_out) {
@@ -1127,6 +1339,57 @@ int pf_get_state(pf_handle* h, int32_t track, void* xs, void* ys, void* cdf) {
   }
   if (cdf)
     PF_CUDA(cudaMemcpy(cdf, (char*)h->C[h->cur] + track * K * h->rs, K * h->rs, cudaMemcpyDeviceToHost), h->err);
+  return PF_OK;
+}
+
+int pf_set_rng_philox(pf_handle* h, const uint64_t* state11) {
+  if (!h || !state11) return PF_EINVAL;
+  if (h->n_tracks != 1 || h->n_shards != 1 || h->split_table) {
+    h->err = "rng='numpy-philox' needs a single unsharded track";
+    return PF_EINVAL;
+  }
+  if (h->tpb != 128 && h->tpb != 256) {
+    h->err = "rng='numpy-philox' runs at 128 or 256 threads per block";
+    return PF_EINVAL;
+  }
+  PF_CUDA(cudaSetDevice(h->device), h->err);
+  if (h->pending) run_complete(h);
+  PF_CUDA(cudaStreamSynchronize(h->stream), h->err);
+  int rc = h->phx.init(state11, h->err);
+  if (rc) return rc;
+  h->philox = true;
+  h->g_F = -1;
+  PF_CUDA(set_fused_smem(h), h->err);
+  PF_CUDA(cudaDeviceSynchronize(), h->err);
+  return PF_OK;
+}
+
+int pf_set_state(pf_handle* h, int32_t track, const void* xs, const void* ys, int64_t frame) {
+  if (!h || track < 0 || track >= h->n_tracks || !xs || !ys || frame < 0 || frame > INT_MAX) return PF_EINVAL;
+  if (h->n_shards > 1) {
+    h->err = "pf_set_state: sharded handles are not supported";
+    return PF_EINVAL;
+  }
+  PF_CUDA(cudaSetDevice(h->device), h->err);
+  if (h->pending) {
+    const int rc = run_complete(h);
+    if (rc && rc != PF_EDEGENERATE) return rc;
+  }
+  PF_CUDA(cudaStreamSynchronize(h->stream), h->err);
+  const size_t K = (size_t)h->Kl;
+  std::vector<unsigned char> buf(K * h->vs);
+  for (size_t k = 0; k < K; ++k) {
+    std::memcpy(buf.data() + k * h->vs, (const char*)xs + k * h->rs, h->rs);
+    std::memcpy(buf.data() + k * h->vs + h->rs, (const char*)ys + k * h->rs, h->rs);
+  }
+  PF_CUDA(cudaMemcpy((char*)h->X[h->cur] + track * K * h->vs, buf.data(), K * h->vs, cudaMemcpyHostToDevice), h->err);
+  // every track enters frame `frame` with identity ancestors; the table-ready
+  // counters restart at the value frame `frame`'s successor expects
+  h->frame_counter = frame;
+  h->ident_next = true;
+  std::vector<unsigned long long> sync((size_t)h->n_tracks * 4, 0ULL);
+  for (int i = 0; i < h->n_tracks; ++i) sync[(size_t)i * 4 + 1] = (unsigned long long)h->n_chunks * (unsigned long long)frame;
+  PF_CUDA(cudaMemcpy(h->tsync, sync.data(), sync.size() * 8, cudaMemcpyHostToDevice), h->err);
   return PF_OK;
 }
 
@@ -1347,8 +1610,40 @@ int pf_shard_ipc_export(pf_handle* h, void* out) {
   return PF_OK;
 }
 
+// direct peer access from h's device to `peer_dev` (the fused kernel reads
+// remote source tiles, the finish kernel stores remote window records)
+static int enable_peer(pf_handle* h, int peer_dev) {
+  if (peer_dev == h->device) return PF_OK;
+  int can = 0;
+  PF_CUDA(cudaDeviceCanAccessPeer(&can, h->device, peer_dev), h->err);
+  if (!can) {
+    h->err = "device " + std::to_string(h->device) + " cannot access device " + std::to_string(peer_dev) +
+             " peer-to-peer (NVLink / PCIe P2P required for a shard on another GPU)";
+    return PF_EINVAL;
+  }
+  PF_CUDA(cudaSetDevice(h->device), h->err);
+  const cudaError_t e = cudaDeviceEnablePeerAccess(peer_dev, 0);
+  if (e == cudaErrorPeerAccessAlreadyEnabled) {
+    cudaGetLastError();  // not an error: clear it
+  } else if (e != cudaSuccess) {
+    h->err = std::string("cudaDeviceEnablePeerAccess: ") + cudaGetErrorString(e);
+    return PF_ECUDA;
+  }
+  return PF_OK;
+}
+
 int pf_shard_set_peer(pf_handle* h, int32_t peer, void* const* ptrs8) {
   if (!h || !ptrs8 || peer < 0 || peer >= h->n_shards || peer == h->shard) return PF_EINVAL;
+  for (int i = 0; i < 8; ++i) {
+    cudaPointerAttributes at{};
+    if (!ptrs8[i] || cudaPointerGetAttributes(&at, ptrs8[i]) != cudaSuccess || at.type != cudaMemoryTypeDevice) {
+      cudaGetLastError();
+      h->err = "pf_shard_set_peer: peer buffer " + std::to_string(i) + " is not device memory";
+      return PF_EINVAL;
+    }
+    const int rc = enable_peer(h, at.device);
+    if (rc) return rc;
+  }
   for (int i = 0; i < 8; ++i) h->peer[peer][i] = ptrs8[i];
   return PF_OK;
 }
@@ -1602,7 +1897,7 @@ int pf_rng_uniforms(uint64_t seed, uint64_t pos, int64_t n, double* out, int32_t
 // NumPy-compatible reference stream on the device (staged parity engine)
 // ---------------------------------------------------------------------------
 struct pf_philox {
-  pfr::PhiloxState* st = nullptr;
+  PhxGen g;
   double* buf = nullptr;
   long long cap = 0;
   int device = 0;
@@ -1616,20 +1911,12 @@ int pf_philox_create(pf_philox** out, const uint64_t* state11, int32_t device) {
   PF_CUDA(cudaSetDevice(device), g_err);
   int rc = init_device_tables(device, g_err);
   if (rc) return rc;
-  pfr::PhiloxState h;
-  h.key[0] = state11[0];
-  h.key[1] = state11[1];
-  for (int i = 0; i < 4; ++i) h.ctr[i] = state11[2 + i];
-  for (int i = 0; i < 4; ++i) h.buf[i] = state11[6 + i];
-  h.pos = (int)state11[10];
   pf_philox* p = new pf_philox();
   p->device = device;
-  if (cudaMalloc(&p->st, sizeof(pfr::PhiloxState)) != cudaSuccess ||
-      cudaMemcpy(p->st, &h, sizeof(h), cudaMemcpyHostToDevice) != cudaSuccess) {
-    g_err = "philox state allocation failed";
-    if (p->st) cudaFree(p->st);
+  if ((rc = p->g.init(state11, g_err))) {
+    p->g.release();
     delete p;
-    return PF_ECUDA;
+    return rc;
   }
   *out = p;
   return PF_OK;
@@ -1638,7 +1925,7 @@ int pf_philox_create(pf_philox** out, const uint64_t* state11, int32_t device) {
 int pf_philox_destroy(pf_philox* p) {
   if (!p) return PF_OK;
   cudaSetDevice(p->device);
-  if (p->st) cudaFree(p->st);
+  p->g.release();
   if (p->buf) cudaFree(p->buf);
   delete p;
   return PF_OK;
@@ -1654,15 +1941,18 @@ static int philox_draw(pf_philox* p, int64_t n, double* out, bool normals) {
     PF_CUDA(cudaMalloc(&p->buf, n * 8), g_err);
     p->cap = n;
   }
-  if (normals)
-    pfs::st_philox_draw<<<1, 1>>>(p->st, n, p->buf, 0, nullptr);
-  else
-    pfs::st_philox_draw<<<1, 1>>>(p->st, 0, nullptr, n, p->buf);
-  PF_CUDA(cudaGetLastError(), g_err);
+  int rc = normals ? p->g.draw(nullptr, n, p->buf, nullptr, g_err) : p->g.uniforms(nullptr, n, p->buf, g_err);
+  if (rc) return rc;
   PF_CUDA(cudaMemcpy(out, p->buf, n * 8, cudaMemcpyDeviceToHost), g_err);
-  return PF_OK;
+  return p->g.check(g_err);
 }
 int pf_philox_normals(pf_philox* p, int64_t n, double* out) { return philox_draw(p, n, out, true); }
+int pf_philox_normals_device(pf_philox* p, int64_t n, double* out_dev, void* stream) {
+  if (!p || !out_dev || n < 0) return PF_EINVAL;
+  if (n == 0) return PF_OK;
+  PF_CUDA(cudaSetDevice(p->device), g_err);
+  return p->g.draw((cudaStream_t)stream, n, out_dev, nullptr, g_err);
+}
 int pf_philox_uniforms(pf_philox* p, int64_t n, double* out) { return philox_draw(p, n, out, false); }
 
 }  // extern "C"

@@ -624,7 +624,8 @@ struct FusedArgs {
   int tile0;          // global index of this handle's first tile
   SrcShards src;
   int H, W, r, Wm;
-  int t;  // frame index in the stream (RNG position, t==0 -> identity ancestors)
+  int t;      // frame index in the stream (RNG position)
+  int ident;  // identity ancestors: frame 0, or a state injected by pf_set_state (no previous table)
   void* X_new;
   void* C_new;
   const double* u_prev;
@@ -649,6 +650,8 @@ struct FusedArgs {
                               //   [1] table-ready counter (+1 per table chunk and frame)
   unsigned long long ready_target;  // frame t > 0 proceeds once tmax[1] >= this (n_chunks * t)
   unsigned long long* trace;  // optional: [tile][8] %globaltimer stamps (track 0)
+  const double2* noise;       // NZ variants: this frame's draws (n, d) per particle (the reference's
+                              //   own stream, generated by pf_philox.cuh), one track
 };
 
 __device__ __forceinline__ unsigned long long gtimer() {
@@ -1083,7 +1086,9 @@ constexpr int fused_min_blocks(int tpb) {
 // DBG: the %globaltimer trace and the ancestor / likelihood capture of the
 // parity tests are compiled only into this instantiation (as runtime checks
 // they cost the production kernel ~10% at C3: registers and code layout)
-template <int MODE, int VPT, int R, bool SH = false, bool PK = true, bool DBG = false>
+// NZ: the frame's normals are read from a.noise (the reference's Philox
+// stream) instead of being drawn from the LCG stream in phase 0
+template <int MODE, int VPT, int R, bool SH = false, bool PK = true, bool DBG = false, bool NZ = false>
 __global__ void __launch_bounds__(PF_TILE / (VPT * R), fused_min_blocks<MODE>(PF_TILE / (VPT * R)))
     pf_fused_frame(FusedArgs a) {
   using real = typename Tr<MODE>::real;
@@ -1190,6 +1195,22 @@ __global__ void __launch_bounds__(PF_TILE / (VPT * R), fused_min_blocks<MODE>(PF
   // overlaps the previous kernel under PDL).  Fast ziggurat path, scaled by
   // d(std), into s_X; slow paths flagged branch-free per thread, then queued
   // and resolved in one CTA-wide pass.
+  if constexpr (NZ) {
+#pragma unroll
+    for (int rr = 0; rr < R; ++rr) {
+      const int l0 = (rr * TPB + tid) * VPT;
+#pragma unroll
+      for (int i = 0; i < VPT; ++i) {
+        if (l0 + i < Tb) {
+          const double2 nz = __ldg(a.noise + base + l0 + i);
+          if constexpr (MODE == M_FP16 && !PK)
+            s_X[l0 + i] = scale_noise_scalar(to_vec<MODE>(nz.x, nz.y), stdv);
+          else
+            s_X[l0 + i] = scale_noise<MODE>(to_vec<MODE>(nz.x, nz.y), stdv);
+        }
+      }
+    }
+  } else {
 #pragma unroll
   for (int rr = 0; rr < R; ++rr) {
     const int v = rr * TPB + tid;
@@ -1236,6 +1257,7 @@ __global__ void __launch_bounds__(PF_TILE / (VPT * R), fused_min_blocks<MODE>(PF
       }
     }
   }
+  }  // LCG draws
   __syncthreads();
   PF_TRACE_DBG(a, 1);
   // ---- warp 0: wait for the previous kernels, read this tile's source window
@@ -1246,7 +1268,7 @@ __global__ void __launch_bounds__(PF_TILE / (VPT * R), fused_min_blocks<MODE>(PF
   uint64_t* s_bar = reinterpret_cast<uint64_t*>(s_misc + 200);
   const bool bulk_ok = ((((size_t)track * Kl) * sizeof(real)) % 16) == 0;
   if (wid == 0 || NW == 1) {
-    if (a.t > 0) {  // acquire the previous frame's table (published before its grid ends)
+    if (!a.ident) {  // acquire the previous frame's table (published before its grid ends)
       if (lane == 0) {
         const unsigned long long* rc = a.tmax + (size_t)track * 4 + 1;
         unsigned long long v;
@@ -1269,17 +1291,18 @@ __global__ void __launch_bounds__(PF_TILE / (VPT * R), fused_min_blocks<MODE>(PF
       }
       __syncwarp();
     } else {
-      pdl_wait();  // frame 0: the likelihood maps / initial positions
+      pdl_wait();  // frame 0 / injected state: the likelihood maps / initial positions
     }
     PF_TRACE_DBG(a, 2);
-    if (a.t > 0) {
+    if (!a.ident) {
       const int2 wn = __ldcg(reinterpret_cast<const int2*>(a.win) + (size_t)track * nl + ltile);
       const int nsrc = wn.y - wn.x + 1;
       const int staged = nsrc <= MS ? 1 : 0;
       if (!SH && staged && bulk_ok && lane == 0) {  // the window is contiguous: one bulk copy
         const uint32_t bb = smem_u32(s_bar);
         const int c0 = wn.x * PF_TILE;
-        const int cnt = min((wn.y + 1) * PF_TILE, K) - c0;
+        // 64-bit: (wn.y + 1) * PF_TILE reaches 2^31 for K near the 2^31-1 bound
+        const int cnt = (int)(min((long long)(wn.y + 1) * PF_TILE, (long long)K) - (long long)c0);
         const uint32_t bytes = (uint32_t)((cnt * (int)sizeof(real) + 15) & ~15);  // C buffers carry 16 B of slack
         asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bb), "r"(1) : "memory");
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -1336,9 +1359,9 @@ __global__ void __launch_bounds__(PF_TILE / (VPT * R), fused_min_blocks<MODE>(PF
   }
   __syncthreads();  // window and slow-path noise visible (and, for every thread, the previous table)
   PF_TRACE_DBG(a, 3);
-  const double u = a.t > 0 ? __ldcg(a.u_prev + track) : 0.0;
+  const double u = !a.ident ? __ldcg(a.u_prev + track) : 0.0;
   int b_lo = 0, b_hi = 0, staged = 0;
-  if (a.t > 0) {
+  if (!a.ident) {
     b_lo = s_int[0];
     b_hi = s_int[1];
     staged = s_int[2];
@@ -1379,7 +1402,7 @@ __global__ void __launch_bounds__(PF_TILE / (VPT * R), fused_min_blocks<MODE>(PF
       constexpr bool FULL = decltype(full_tag)::value;
       auto in_tile = [&](int i) -> bool { return FULL || l0 + i < Tb; };
       int anc[VPT];  // global ancestor index
-      if (a.t == 0 || (!FULL && l0 >= Tb)) {  // frame 0: identity ancestors
+      if (a.ident || (!FULL && l0 >= Tb)) {  // frame 0 / injected state: identity ancestors
 #pragma unroll
         for (int i = 0; i < VPT; ++i) anc[i] = base + l0 + i;
       } else {
@@ -1706,7 +1729,7 @@ __global__ void __launch_bounds__(PF_TILE / (VPT * R), fused_min_blocks<MODE>(PF
   PF_TRACE_DBG(a, 5);
   // complete only after the previous grid (keeps grid completion in stream
   // order: the next table reuses the exchange counters and records)
-  if (a.t > 0 && tid == 0) pdl_wait();
+  if (!a.ident && tid == 0) pdl_wait();
 }
 
 // ------------------------------------------------------------------------
@@ -1737,6 +1760,7 @@ struct TableArgs {
   double* roots;                // per track x chunk x 3: estimate subtree roots
   unsigned long long* trace;    // optional: [chunk][8] %globaltimer stamps (track 0)
   int2* win;                    // [track][tile]: source window of each destination tile (next frame)
+  const double* u_in;           // optional: the frame's uniform (reference Philox stream), else the LCG's
 };
 
 // canonical pairwise accumulation over a power-of-two run (binary counter)
@@ -1825,7 +1849,7 @@ __global__ void __launch_bounds__(1024) pf_tile_table(TableArgs a) {
   PF_TRACE_DBG(a, 0);
   pdl_launch_dependents();
   // the frame's resampling uniform: stream position t(2K+1)+2K
-  const double u = pfr::uniform_of(a.ua * a.x0[track] + a.uc);
+  const double u = a.u_in ? *a.u_in : pfr::uniform_of(a.ua * a.x0[track] + a.uc);
   const double scale = ldexp(1.0, a.Q - FB);
   const double Kd = __ll2double_rn(a.K);
   const double invK = __ddiv_rn(1.0, Kd);

@@ -118,17 +118,11 @@ __device__ __forceinline__ double normal_of(uint64_t w, const uint32_t* ki_hi, c
 }
 
 // ---------------------------------------------------------------------------
-// NumPy-compatible reference stream (Generator(Philox(seed)), filter.py:71-82)
-// for the staged parity engine: Philox4x64-10 with NumPy's counter/buffer
-// semantics, NumPy's ziggurat (low-bit layout), and glibc's log1p restated
-// from its x86-64 FMA variant (oracle/rng.py log1p_glibc).  Sequential by
-// nature (variable consumption), one thread per stream.
+// NumPy-compatible reference stream (Generator(Philox(seed)), filter.py:71-82):
+// Philox4x64-10 with NumPy's counter semantics and glibc's log1p restated from
+// its x86-64 FMA variant (oracle/rng.py log1p_glibc).  The stream itself is
+// generated in parallel by pf_philox.cuh.
 // ---------------------------------------------------------------------------
-struct PhiloxState {
-  unsigned long long key[2], ctr[4], buf[4];
-  int pos;
-};
-
 __device__ __forceinline__ void philox_block(const unsigned long long ctr_in[4], const unsigned long long key_in[2],
                                              unsigned long long out[4]) {
   unsigned long long c0 = ctr_in[0], c1 = ctr_in[1], c2 = ctr_in[2], c3 = ctr_in[3];
@@ -152,17 +146,6 @@ __device__ __forceinline__ void philox_block(const unsigned long long ctr_in[4],
   out[2] = c2;
   out[3] = c3;
 }
-
-__device__ __forceinline__ unsigned long long philox_next(PhiloxState& st) {
-  if (st.pos < 4) return st.buf[st.pos++];
-  if (++st.ctr[0] == 0)
-    if (++st.ctr[1] == 0)
-      if (++st.ctr[2] == 0) ++st.ctr[3];
-  philox_block(st.ctr, st.key, st.buf);
-  st.pos = 1;
-  return st.buf[0];
-}
-__device__ __forceinline__ double philox_double(PhiloxState& st) { return uniform_of(philox_next(st)); }
 
 // glibc 2.39 log1p (x86-64 FMA variant), domain -1 < x <= 0.41422
 __device__ double log1p_glibc(double x) {
@@ -216,37 +199,6 @@ __device__ double log1p_glibc(double x) {
   if (k == 0) return __dsub_rn(f, __dsub_rn(hfsq, t));
   const double klo = __fma_rn(kf, LN2_LO, c);
   return __fma_rn(kf, LN2_HI, -__dsub_rn(__dsub_rn(hfsq, __dadd_rn(klo, t)), f));
-}
-
-// numpy random_standard_normal over the Philox stream (distributions.c)
-__device__ double numpy_normal(PhiloxState& st) {
-  for (;;) {
-    unsigned long long r = philox_next(st);
-    const unsigned idx = (unsigned)(r & 0xff);
-    r >>= 8;
-    const unsigned sign = (unsigned)(r & 1);
-    const unsigned long long rabs = (r >> 1) & kMask52;
-    double x = pfm::dmul((double)rabs, __longlong_as_double((long long)PF_ZIG_WI_BITS[idx]));
-    if (sign) x = -x;
-    if (rabs < PF_ZIG_KI[idx]) return x;
-    if (idx == 0) {
-      for (;;) {
-        const double xx = pfm::dmul(-kZigInvR, log1p_glibc(-philox_double(st)));
-        const double yy = -log1p_glibc(-philox_double(st));
-        if (pfm::dadd(yy, yy) > pfm::dmul(xx, xx))
-          return ((rabs >> 8) & 1) ? -pfm::dadd(kZigR, xx) : pfm::dadd(kZigR, xx);
-      }
-    } else {
-      const double fi0 = __longlong_as_double((long long)PF_ZIG_FI_BITS[idx - 1]);
-      const double fi1 = __longlong_as_double((long long)PF_ZIG_FI_BITS[idx]);
-      // glibc exp vs the portable exp64 here only decides a comparison; they
-      // differ by at most an ulp, so a flip needs the uniform to land within
-      // ~2^-52 of the wedge boundary (documented in DESIGN.md)
-      if (pfm::dadd(pfm::dmul(pfm::dsub(fi0, fi1), philox_double(st)), fi1) <
-          pfm::exp64(pfm::dmul(pfm::dmul(-0.5, x), x)))
-        return x;
-    }
-  }
 }
 
 }  // namespace pfr

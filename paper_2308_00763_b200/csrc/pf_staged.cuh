@@ -291,15 +291,6 @@ __global__ void st_rng_uniforms(unsigned long long x0, unsigned long long pos, l
   out[i] = pfr::uniform_of(pfr::word_at(x0, pos + (unsigned long long)i));
 }
 
-// NumPy-compatible stream: n normals then m uniforms, sequentially (1 thread)
-__global__ void st_philox_draw(pfr::PhiloxState* stp, long long n_normals, double* normals, long long n_uniforms,
-                               double* uniforms) {
-  pfr::PhiloxState st = *stp;
-  for (long long i = 0; i < n_normals; ++i) normals[i] = pfr::numpy_normal(st);
-  for (long long i = 0; i < n_uniforms; ++i) uniforms[i] = pfr::philox_double(st);
-  *stp = st;
-}
-
 template <int MODE>
 __global__ void fill_start(long long n, void* X, double x0, double y0) {
   using vec = typename Tr<MODE>::vec;

@@ -383,7 +383,10 @@ class Filter:
                  params: Optional[ModelParams] = None, template: Optional[PixelTemplate] = None,
                  start_hint: Optional[Tuple[float, float]] = None, n_tracks: int = 1,
                  seeds: Optional[Sequence[int]] = None, n_videos: int = 1, tpb: Optional[int] = None,
-                 device: int = 0):
+                 device: int = 0, rng: str = "lcg"):
+        if rng not in ("lcg", "numpy-philox"):
+            raise ValueError(f"unknown rng {rng!r} (expected 'lcg' or 'numpy-philox')")
+        self.rng = rng
         self.mode = _mode(mode)
         _validate_k(K, self.mode)
         self.K = int(K)
@@ -421,6 +424,17 @@ class Filter:
         N.check(rc, L.pf_global_error)
         self._h = h
         self.device = device
+        if rng == "numpy-philox":
+            # the reference's stream (filter.py:71-82): NumPy seeds the Philox
+            # key (SeedSequence) on the host, the draws are generated on the device
+            st = np.random.Philox(int(self.seeds[0])).state
+            state = np.array(list(st["state"]["key"]) + list(st["state"]["counter"]) + list(st["buffer"]) +
+                             [st["buffer_pos"]], dtype=np.uint64)
+            rc = L.pf_set_rng_philox(h, N.ptr(state))
+            if rc:
+                msg = self._err().decode()
+                self.close()
+                raise ValueError(msg)
 
     def _err(self):
         return N.lib().pf_last_error(self._h)
@@ -441,32 +455,100 @@ class Filter:
             self.start_hint = (float(start_hint[0]), float(start_hint[1]))
         N.check(N.lib().pf_reset(self._h, *self.start_hint), self._err)
 
-    def _frames_arg(self, frames, per_video_ndim: int):
-        """Host uint8 array -> (pointer, on_device=0, keepalive); CUDA tensors pass through."""
-        if hasattr(frames, "data_ptr") and getattr(frames, "is_cuda", False):
-            return C.c_void_p(frames.data_ptr()), 1, frames
-        arr = np.ascontiguousarray(np.asarray(frames, dtype=np.uint8))
-        return C.c_void_p(arr.ctypes.data), 0, arr
+    def _frames_arg(self, frames, n_frames: Optional[int]):
+        """Validate frames against the handle and return (pointer, on_device, keepalive, n_frames).
 
-    def run_frames(self, frames, n_frames: int) -> np.ndarray:
-        """frames: [n_videos][F][H][W] (or [F][H][W] with one video)."""
-        p, on_dev, keep = self._frames_arg(frames, 3)
-        traj = np.empty((self.n_tracks, n_frames, 2), dtype=np.float64)
-        rc = N.lib().pf_run(self._h, p, int(n_frames), on_dev, N.ptr(traj))
-        if rc == N.PF_EDEGENERATE:
-            raise DegeneracyError(self._err().decode(), N.lib().pf_degenerate_frame(self._h))
-        N.check(rc, self._err)
+        Accepted: [n_videos][F][H][W] uint8, or [F][H][W] with one video
+        (n_frames=None); for one frame ([n_videos][H][W] / [H][W]) pass
+        n_frames=1 with the frame axis absent.  Host arrays must be uint8
+        (C-contiguous copies are made as needed); CUDA tensors must be uint8,
+        contiguous and on the handle's device (they are read in place)."""
+        H, W, nv = self.height, self.width, self.n_videos
+        is_cuda = hasattr(frames, "data_ptr") and getattr(frames, "is_cuda", False)
+        shape = tuple(int(v) for v in frames.shape)
+        if n_frames == 1 and len(shape) in (2, 3) and shape[-2:] == (H, W) and (len(shape) == 2 or shape[0] == nv):
+            shape = (nv, 1, H, W) if len(shape) == 3 else (1, H, W)
+        if len(shape) == 3 and nv == 1:
+            shape = (1,) + shape
+        if len(shape) != 4 or shape[0] != nv or shape[2:] != (H, W) or shape[1] < 1:
+            want = f"({nv}, F, {H}, {W})" + (f" or (F, {H}, {W})" if nv == 1 else "")
+            raise ValueError(f"frames of shape {tuple(frames.shape)} do not match the filter: expected {want}")
+        F = shape[1]
+        if n_frames is not None and n_frames != F:
+            raise ValueError(f"expected {n_frames} frame(s), got {F}")
+        if is_cuda:
+            import torch
+
+            if frames.dtype != torch.uint8:
+                raise ValueError(f"frames must be uint8, got {frames.dtype}")
+            if not frames.is_contiguous():
+                raise ValueError("CUDA frames must be contiguous")
+            if frames.device.index != self.device:
+                raise ValueError(f"CUDA frames are on device {frames.device.index}, the filter on {self.device}")
+            return C.c_void_p(frames.data_ptr()), 1, frames, F
+        arr = np.asarray(frames)
+        if arr.dtype != np.uint8:
+            raise ValueError(f"frames must be uint8, got {arr.dtype}")
+        arr = np.ascontiguousarray(arr)
+        return C.c_void_p(arr.ctypes.data), 0, arr, F
+
+    def _launch(self, frames, n_frames: Optional[int]) -> np.ndarray:
+        p, on_dev, keep, F = self._frames_arg(frames, n_frames)
+        traj = np.empty((self.n_tracks, F, 2), dtype=np.float64)
+        L = N.lib()
+        if on_dev:
+            # device frames may still be in flight on torch's current stream:
+            # the library stream is ordered after it (stream-ordered call)
+            import torch
+
+            stream = torch.cuda.current_stream(self.device).cuda_stream
+            rc = L.pf_run_async(self._h, p, F, 1, N.ptr(traj), C.c_void_p(stream))
+            if rc == N.PF_OK:
+                rc = L.pf_sync(self._h)
+        else:
+            rc = L.pf_run(self._h, p, F, 0, N.ptr(traj))
         del keep
+        if rc == N.PF_EDEGENERATE:
+            raise DegeneracyError(self._err().decode(), L.pf_degenerate_frame(self._h))
+        N.check(rc, self._err)
         return traj
 
+    def run_frames(self, frames, n_frames: Optional[int] = None) -> np.ndarray:
+        """frames: [n_videos][F][H][W] (or [F][H][W] with one video) -> [n_tracks][F][2]."""
+        return self._launch(frames, n_frames)
+
     def run(self, frames) -> np.ndarray:
-        n_frames = (frames.shape[-3])
-        traj = self.run_frames(frames, n_frames)
+        traj = self._launch(frames, None)
         return traj[0] if self.n_tracks == 1 else traj
 
     def step(self, frame):
-        est = self.run_frames(frame, 1)[:, 0, :]
+        """One frame ([H][W], or [n_videos][H][W]) -> the estimate(s) (filter.py:617-654)."""
+        est = self._launch(frame, 1)[:, 0, :]
         return (float(est[0, 0]), float(est[0, 1])) if self.n_tracks == 1 else est
+
+    def run_async(self, frames, traj_out, stream=None):
+        """Stream-ordered run of CUDA frames into a CUDA float64 tensor traj_out
+        [n_tracks][F][2]: queued behind `stream` (default: torch's current
+        stream), which later work can consume without a host synchronisation.
+        Call sync() to wait and to surface a DegeneracyError."""
+        import torch
+
+        p, on_dev, keep, F = self._frames_arg(frames, None)
+        if not on_dev:
+            raise ValueError("run_async takes CUDA frames")
+        if (not getattr(traj_out, "is_cuda", False) or traj_out.dtype != torch.float64 or not traj_out.is_contiguous()
+                or tuple(traj_out.shape) != (self.n_tracks, F, 2)):
+            raise ValueError(f"traj_out must be a contiguous CUDA float64 tensor of shape ({self.n_tracks}, {F}, 2)")
+        s = (stream or torch.cuda.current_stream(self.device)).cuda_stream
+        self._async_keep = (keep, traj_out)
+        N.check(N.lib().pf_run_async(self._h, p, F, 1, C.c_void_p(traj_out.data_ptr()), C.c_void_p(s)), self._err)
+
+    def sync(self):
+        rc = N.lib().pf_sync(self._h)
+        self._async_keep = None
+        if rc == N.PF_EDEGENERATE:
+            raise DegeneracyError(self._err().decode(), N.lib().pf_degenerate_frame(self._h))
+        N.check(rc, self._err)
 
     def likelihood_maps(self, frames) -> np.ndarray:
         """[F, H+2r, W+2r] per-position likelihood maps of host frames (mode dtype)."""
@@ -498,6 +580,18 @@ class Filter:
         N.check(N.lib().pf_get_state(self._h, track, N.ptr(xs), N.ptr(ys), N.ptr(cdf)), self._err)
         return xs, ys, cdf
 
+    def set_state(self, xs, ys, frame: int, track: int = 0):
+        """Inject post-resample positions entering frame `frame` (teacher forcing):
+        the next frame uses identity ancestors and frame `frame`'s draws
+        (pf_set_state; the reference's seam is a stage_hook editing ParticleSet)."""
+        dt = _DTYPE[self.mode]
+        with np.errstate(over="ignore"):
+            x = np.ascontiguousarray(np.asarray(xs).astype(dt, copy=False))
+            y = np.ascontiguousarray(np.asarray(ys).astype(dt, copy=False))
+        if x.shape != (self.K,) or y.shape != (self.K,):
+            raise ValueError(f"xs and ys must have shape ({self.K},)")
+        N.check(N.lib().pf_set_state(self._h, int(track), N.ptr(x), N.ptr(y), int(frame)), self._err)
+
     def enable_debug(self):
         N.check(N.lib().pf_get_debug(self._h, 0, None, None), self._err)
 
@@ -511,14 +605,16 @@ class Filter:
 def run(video: Video, K: int, mode, seed: int, workers: int = 1, params: Optional[ModelParams] = None,
         template: Optional[PixelTemplate] = None, start_hint: Optional[Tuple[float, float]] = None,
         stage_hook: Optional[Callable] = None, tpb: Optional[int] = None, device: int = 0,
-        engine: Optional[str] = None) -> RunResult:
+        engine: Optional[str] = None, rng: str = "lcg") -> RunResult:
     """Track through a whole video (filter.py:591-662).
 
     engine="fused" (default without stage_hook): one fused kernel + one tile
     table kernel per frame, FP16 is the stabilised variant.  engine="staged"
     (forced by stage_hook): one device call per reference stage, reference
     semantics in every mode, draws from `RngStream` (resolved at call time,
-    so it can be swapped, as in the reference)."""
+    so it can be swapped, as in the reference).  rng="numpy-philox" draws
+    from the reference's own stream, Generator(Philox(seed)), on the device
+    (both engines)."""
     mode = _mode(mode)
     params = params or ModelParams()
     template = template if template is not None else disk_template(params.disk_radius)
@@ -530,7 +626,8 @@ def run(video: Video, K: int, mode, seed: int, workers: int = 1, params: Optiona
     if engine == "fused":
         if stage_hook is not None:
             raise ValueError("stage_hook requires engine='staged'")
-        f = Filter(K, mode, video.width, video.height, seed, params, template, start_hint, tpb=tpb, device=device)
+        f = Filter(K, mode, video.width, video.height, seed, params, template, start_hint, tpb=tpb, device=device,
+                   rng=rng)
         try:
             t0 = time.perf_counter()
             try:
@@ -549,7 +646,9 @@ def run(video: Video, K: int, mode, seed: int, workers: int = 1, params: Optiona
     if engine != "staged":
         raise ValueError(f"unknown engine {engine!r}")
     eng = make_engine(mode, params, template, device=device)
-    rng = RngStream(seed)
+    if rng not in ("lcg", "numpy-philox"):
+        raise ValueError(f"unknown rng {rng!r} (expected 'lcg' or 'numpy-philox')")
+    stream = PhiloxRngStream(seed, device) if rng == "numpy-philox" else RngStream(seed)
     ps = eng.init(K, start_hint)
     trajectory = np.empty((video.frame_count, 2), dtype=np.float64)
     stage_ms = {name: 0.0 for name in STAGES}
@@ -558,7 +657,7 @@ def run(video: Video, K: int, mode, seed: int, workers: int = 1, params: Optiona
         frame = video.frames[t]
         try:
             t0 = time.perf_counter()
-            eng.propagate(ps, rng.normals(K))
+            eng.propagate(ps, stream.normals(K))
             t1 = time.perf_counter()
             if stage_hook:
                 stage_hook(t, "propagate", ps)
@@ -579,7 +678,7 @@ def run(video: Video, K: int, mode, seed: int, workers: int = 1, params: Optiona
             t5 = time.perf_counter()
             if stage_hook:
                 stage_hook(t, "normalize", ps)
-            eng.resample(ps, rng.uniform())
+            eng.resample(ps, stream.uniform())
             t6 = time.perf_counter()
             if stage_hook:
                 stage_hook(t, "resample", ps)

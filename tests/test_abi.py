@@ -65,3 +65,15 @@ def test_python_api_validation_mirrors_reference():
     with pytest.raises(ValueError, match="even"):
         F._validate_k(3, F.PrecisionMode.FP16_PACKED)
     F._validate_k(1 << 24, F.PrecisionMode.FP16_PACKED)
+
+
+def test_pipes_library_exports_declared_symbols():
+    from paper_2308_00763_b200 import pipes
+
+    src = open(os.path.join(ROOT, "include", "pf_pipes.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    names = set(re.findall(r"\b(pf_[a-z0-9_]+)\s*\(", src))
+    L = pipes.lib()
+    assert all(hasattr(L, n) for n in names)
+    assert names == {s[0] for s in pipes.SIGNATURES}
+    assert L.pf_pipe_count() == 12 and L.pf_pipe_name(0) == b"hfma2"

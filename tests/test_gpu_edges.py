@@ -18,6 +18,11 @@ def _pf():
     return pf
 
 
+@pytest.fixture(scope="module")
+def pf():
+    return _pf()
+
+
 @pytest.mark.parametrize("mode", ["fp64", "fp32", "fp16-packed"])
 @pytest.mark.parametrize("W,H,r", [(1, 1, 5), (2, 7, 1), (64, 48, 20), (33, 17, 1)])
 def test_shapes_and_radii(mode, W, H, r):
@@ -75,3 +80,54 @@ def test_chunked_host_upload_equals_device_frames(mode, W, F):
     pinned = f.run_frames(torch.from_numpy(frames).pin_memory().numpy(), F)
     f.close()
     assert np.array_equal(dev, host) and np.array_equal(dev, pinned)
+
+
+def test_frame_validation(pf):
+    import torch
+
+    f = pf.Filter(2048, "fp32", 64, 48, 1)
+    good = np.zeros((3, 48, 64), dtype=np.uint8)
+    f.run(good)
+    for bad in (np.zeros((3, 64, 48), np.uint8), np.zeros((3, 48, 63), np.uint8), np.zeros((48, 64), np.uint8),
+                np.zeros((2, 3, 48, 64), np.uint8), np.zeros((0, 48, 64), np.uint8)):
+        with pytest.raises(ValueError):
+            f.run(bad)
+    with pytest.raises(ValueError):
+        f.run(good.astype(np.float32))
+    with pytest.raises(ValueError):
+        f.step(np.zeros((48, 65), np.uint8))
+    t = torch.zeros((3, 48, 128), dtype=torch.uint8, device="cuda")[:, :, ::2]
+    with pytest.raises(ValueError):  # non-contiguous
+        f.run(t)
+    with pytest.raises(ValueError):
+        f.run(torch.zeros((3, 48, 64), dtype=torch.int16, device="cuda"))
+    assert f.step(np.zeros((48, 64), np.uint8)) is not None
+    f.close()
+
+
+def test_stream_ordered_run(pf):
+    # frames produced by torch work still in flight on a side stream: the
+    # stream-ordered call waits for them; the trajectory lands on the device
+    import torch
+
+    F, K = 6, 20_000
+    frames, _ = rp.generate_video(rp.Params(), F, 128, 128, (64.0, 64.0), 42)
+    ref = pf.Filter(K, "fp16-packed", 128, 128, 42).run(frames)
+    f = pf.Filter(K, "fp16-packed", 128, 128, 42)
+    side = torch.cuda.Stream()
+    src = torch.from_numpy(frames).pin_memory()
+    with torch.cuda.stream(side):
+        torch.cuda._sleep(20_000_000)  # keep the side stream busy before the copy lands
+        dev = src.to("cuda", non_blocking=True)
+        traj = torch.empty((1, F, 2), dtype=torch.float64, device="cuda")
+        f.run_async(dev, traj)
+        out = traj.cpu()  # ordered after the run on the same stream
+    f.sync()
+    assert np.array_equal(out.numpy()[0], ref)
+    # the blocking API with device frames orders itself after torch's current stream
+    with torch.cuda.stream(side):
+        torch.cuda._sleep(20_000_000)
+        dev2 = src.to("cuda", non_blocking=True)
+        f.reset()
+        assert np.array_equal(f.run(dev2), ref)
+    f.close()

@@ -136,3 +136,73 @@ def test_split_table_equals_chunked(pf, mode, K, monkeypatch):
     monkeypatch.setenv("PF_FORCE_SPLIT_TABLE", "1")
     two = pf.Filter(K, mode, 96, 80, 5, start_hint=(40.0, 30.0)).run(frames)
     assert np.array_equal(one, two)
+
+
+def _n_gpus():
+    import torch
+
+    return torch.cuda.device_count()
+
+
+def _nccl_worker(rank, world, port, K, mode, out_dir):
+    import torch
+    import torch.distributed as dist
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    torch.cuda.set_device(rank)
+    dist.init_process_group("nccl", rank=rank, world_size=world, device_id=torch.device("cuda", rank))
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    from oracle import reference_port as rp_
+    from paper_2308_00763_b200.sharded import DistShard
+
+    frames, _ = rp_.generate_video(rp_.Params(), 6, 96, 80, (40.0, 30.0), 17)
+    sh = DistShard(K, mode, 96, 80, 5, start_hint=(40.0, 30.0), device=rank)  # NCCL all-gathers
+    traj = sh.run(frames)
+    np.save(os.path.join(out_dir, f"traj{rank}.npy"), traj)
+    sh.close()
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.skipif("_n_gpus() < 2")
+@pytest.mark.parametrize("mode", ["fp16", "fp64"])
+def test_two_gpus_nccl_bit_identical(pf, mode, tmp_path):
+    # one shard per GPU: NCCL all-gathers on the library stream, remote
+    # ancestors read over CUDA-IPC peer mappings (NVLink) -- must equal the
+    # single-device filter bit for bit
+    import torch.multiprocessing as mp
+
+    K = 30_001
+    frames, _ = rp.generate_video(rp.Params(), 6, 96, 80, (40.0, 30.0), 17)
+    one = pf.Filter(K, mode, 96, 80, 5, start_hint=(40.0, 30.0)).run(frames)
+    mp.spawn(_nccl_worker, args=(2, _free_port(), K, mode, str(tmp_path)), nprocs=2, join=True)
+    for r in range(2):
+        assert np.array_equal(np.load(tmp_path / f"traj{r}.npy"), one)
+
+
+@pytest.mark.skipif("_n_gpus() < 2")
+def test_local_shards_on_distinct_devices(pf):
+    # shards on different GPUs in one process: pf_shard_set_peer enables peer
+    # access, the fused kernels read remote source tiles directly
+    from paper_2308_00763_b200.sharded import LocalShards
+
+    frames, _ = rp.generate_video(rp.Params(), 5, 96, 80, (40.0, 30.0), 17)
+    n = min(_n_gpus(), 4)
+    one = pf.Filter(50_000, "fp32", 96, 80, 5, start_hint=(40.0, 30.0)).run(frames)
+    sh = LocalShards(50_000, "fp32", 96, 80, 5, n_shards=n, start_hint=(40.0, 30.0), devices=list(range(n)))
+    assert np.array_equal(sh.run(frames), one)
+    sh.close()
+
+
+def test_set_peer_rejects_host_memory(pf):
+    # peer buffers must be device memory (pf_shard_set_peer checks each pointer)
+    import ctypes
+
+    from paper_2308_00763_b200.sharded import _Shard
+
+    s = _Shard(10_000, "fp32", 64, 64, 1, 2, 0)
+    host = [ctypes.addressof(ctypes.c_char.from_buffer(bytearray(64))) for _ in range(8)]
+    with pytest.raises(Exception):
+        s.set_peer(1, host)
+    s.close()

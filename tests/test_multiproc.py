@@ -135,3 +135,32 @@ def test_shard_layout_matches_library_rule():
             assert st & (st - 1) == 0
             assert sum(c for _, c in lay) == K and all(c > 0 for _, c in lay)
             assert [f for f, _ in lay] == [r * st * 1024 for r in range(S)]
+
+
+def test_bench_relaunches_under_torchrun(monkeypatch):
+    # `python bench.py --gpus N` (no launcher) re-runs itself under torchrun,
+    # one rank per GPU on a 127.0.0.1 rendezvous
+    import sys as _sys
+
+    import bench
+
+    calls = []
+    monkeypatch.setattr(bench.subprocess, "call", lambda cmd: calls.append(cmd) or 0)
+    monkeypatch.delenv("WORLD_SIZE", raising=False)
+    monkeypatch.setattr(_sys, "argv", ["bench.py", "--gpus", "4", "--steps", "3"])
+    bench.main()
+    (cmd,) = calls
+    assert cmd[1:3] == ["-m", "torch.distributed.run"]
+    assert "--nproc-per-node=4" in cmd and "--master-addr=127.0.0.1" in cmd
+    assert cmd[-4:] == ["--gpus", "4", "--steps", "3"]
+
+
+def test_bench_rejects_world_size_mismatch(monkeypatch):
+    import sys as _sys
+
+    import bench
+
+    monkeypatch.setenv("WORLD_SIZE", "2")
+    monkeypatch.setattr(_sys, "argv", ["bench.py", "--gpus", "4"])
+    with pytest.raises(SystemExit):
+        bench.main()

@@ -98,3 +98,47 @@ def test_ancestors_match_flat_systematic_resampling():
     ref = np.minimum(np.searchsorted(flat, pts, side="left"), 2999)
     # identical except where a point falls within rounding of a boundary
     assert np.mean(anc == ref) > 0.999
+
+
+def test_oracle_set_state_reproduces_the_run():
+    # pf_set_state semantics: the post-resample state entering frame t
+    # (positions gathered through frame t's ancestors) + identity ancestors
+    frames, _ = rp.generate_video(rp.Params(), 6, 128, 128, (64.0, 64.0), 42)
+    for mode in ("fp64", "fp32", "fp16"):
+        tr = fused.FusedTrack(mode, 5000, 128, 128, 42, (64.0, 64.0))
+        for t in range(4):
+            tr.step(tr.loglik_map(frames[t]))
+        xs, ys = tr.xs.copy(), tr.ys.copy()
+        e4 = tr.step(tr.loglik_map(frames[4]))
+        anc4 = tr.last_ancestors  # frame 4's ancestors into frame 3's positions
+        e5 = tr.step(tr.loglik_map(frames[5]))
+        inj = fused.FusedTrack(mode, 5000, 128, 128, 42, (64.0, 64.0))
+        inj.set_state(xs[anc4], ys[anc4], 4)
+        assert inj.step(inj.loglik_map(frames[4])) == e4
+        assert inj.step(inj.loglik_map(frames[5])) == e5
+
+
+@pytest.mark.parametrize("mode,tol", [("fp64", 1e-9), ("fp32", 1e-4)])
+def test_oracle_teacher_forced_per_frame(mode, tol):
+    # the fused algorithm given the reference's state entering each frame
+    # reproduces the reference's estimate of that frame (SURVEY 8d
+    # "teacher-forced per frame"); the GPU version at C2/C3 sizes is
+    # tests/test_gpu_teacher.py
+    frames, _ = rp.generate_video(rp.Params(), 40, 128, 128, (64.0, 64.0), 42)
+    K = 20_000
+    eng = rp.make_engine(mode, rp.Params(), rp.disk_offsets(5))
+    stream = rng.LcgStream(42)
+    s = eng.init(K, (64.0, 64.0))
+    worst = 0.0
+    for t in range(40):
+        xs_in, ys_in = s.xs[s.ancestors], s.ys[s.ancestors]
+        eng.propagate(s, stream.normals(K))
+        eng.likelihoods(s, frames[t])
+        eng.normalize_and_scan(s, eng.weight_update(s, eng.max_loglik(s)))
+        ref = np.array(eng.estimate(s))
+        eng.resample(s, stream.uniform())
+        tr = fused.FusedTrack(mode, K, 128, 128, 42, (64.0, 64.0))
+        tr.set_state(xs_in, ys_in, t)
+        est = np.array(tr.step(tr.loglik_map(frames[t])))
+        worst = max(worst, float(np.max(np.abs(est - ref) / np.abs(ref))))
+    assert worst <= tol, worst
