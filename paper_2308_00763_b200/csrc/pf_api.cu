@@ -344,6 +344,10 @@ struct pf_handle {
   // uniform come from the reference's own stream, generated before the frames
   bool philox = false;
   PhxGen phx;
+  // the next fused launch follows a kernel whose results it reads without a
+  // grid dependency wait (likelihood maps, Philox draws): launch it without
+  // programmatic overlap
+  bool serialize_next = false;
   double* noise_all = nullptr;  // [F][K][2]
   size_t noise_cap = 0;
   double* u_all = nullptr;  // [F]
@@ -930,6 +934,7 @@ static int launch_maps(pf_handle* h, const uint8_t* dframes, int F, int f0 = 0, 
   } else
     pfk::pf_map_half<<<grid, 256, h->map_smem, h->stream>>>(a);
   h->launches += 1;
+  h->serialize_next = true;
   PF_CUDA(cudaGetLastError(), h->err);
   return PF_OK;
 }
@@ -994,9 +999,13 @@ static int launch_frame(pf_handle* h, const void* map_slot, long long map_video_
   const size_t tr_frame = (size_t)(h->n_tiles + h->n_chunks) * 8;
   a.trace = (h->tracing && h->d_trace) ? h->d_trace + (size_t)traj_index * tr_frame : nullptr;
   a.noise = h->philox ? reinterpret_cast<const double2*>(h->noise_all + (size_t)traj_index * 2 * h->K) : nullptr;
+  // a non-identity frame acquires the previous table's release counter instead
+  // of waiting on its predecessor grid, so it may overlap only a table kernel:
+  // after the maps (or draw) kernels it is launched stream-ordered
   PF_CUDA(launch_pdl(h, (const void*)fused_kernel(h), dim3(h->nl, h->n_tracks), dim3(h->tpb), h->fused_smem, a,
-                     !ordered),
+                     !ordered && !h->serialize_next),
           h->err);
+  h->serialize_next = false;
   PF_CUDA(cudaGetLastError(), h->err);
   if (h->n_shards > 1) {  // the sharded tables run after the host's collectives (pf_shard_*)
     h->launches += 1;
