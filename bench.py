@@ -220,7 +220,9 @@ def run_reference_arm(args, cfg, rank, world):
         arm.close()
     tot = sum(times)
     value = procs * K * args.steps / tot
-    sample = (f"oracle port of halfpf {mode} wide engine (direct (K,81) gather, NumPy, 1 thread/process), "
+    sample = (f"oracle port of halfpf {mode} wide engine (oracle/reference_port.py: a NumPy restatement pinned "
+              f"bit-exactly to halfpf, not halfpf itself -- /root/reference is absent on the GPU box; direct (K,81) "
+              f"likelihood gather in chunks of 65536 particles, NumPy, 1 thread/process), "
               f"{procs} processes x 1 frame of {K} particles per step on {cfg['W']}x{cfg['H']}; "
               f"reference FP16 is pure-Python emulation, degenerate at K>=65536, so FP32 is the CPU arm")
     line = {
@@ -624,7 +626,8 @@ def main():
         mode = "fp32" if prec.startswith("fp16") else prec
         rate, info = cpu_sample(cfg, mode=mode, procs=1, frames=2)
         cpu = {"value": rate, "unit": UNIT, "cores": 1, "kind": "port",
-               "sample": (f"oracle port of halfpf {mode} wide engine (direct (K,81) gather), {info['frames']} frames "
+               "sample": (f"oracle port of halfpf {mode} wide engine (oracle/reference_port.py, a restatement pinned "
+                          f"to halfpf; direct (K,81) gather chunked at 65536), {info['frames']} frames "
                           f"of {info['K']} particles on the C2 video ({info['seconds']:.1f} s); reference FP16 is "
                           f"pure-Python emulation and degenerate at K>=65536"),
                "cpu": cpu_model()}

@@ -264,7 +264,10 @@ class FusedTrack:
         if noise is None:
             base = self.t * (2 * K + 1)
             words = rng.lcg_words(self.x0, base, 2 * K)
-            noise = rng.normals_from_lcg_words(words).reshape(K, 2)
+            if self.mode == "fp16":  # precision-matched binary16 draws (rng.normals16_from_lcg_words)
+                noise = rng.normals16_from_lcg_words(words).reshape(K, 2)
+            else:
+                noise = rng.normals_from_lcg_words(words).reshape(K, 2)
             u = (rng.lcg_word(self.x0, base + 2 * K) >> 11) * rng.TWO_M53
         anc = self.ancestors()
         self.last_ancestors = anc

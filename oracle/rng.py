@@ -270,6 +270,31 @@ def normals_from_lcg_words(words: np.ndarray) -> np.ndarray:
     return x
 
 
+# binary16 modes of the fused kernels ("precision-matched" draws): the same
+# word stream, the ziggurat fast path evaluated in binary32 on the word's high
+# 32 bits -- idx = bits 56..63, sign = bit 55, rabs = bits 32..54 (23 bits) --
+# with tables ki32 = ki >> 29 and wi32 = RN32(wi * 2^29); x = RN32(rabs * wi32),
+# then RN16.  A word failing the binary32 fast test takes the full f64 slow
+# path of the same word (_zig_slow_lcg), rounded once to binary16.
+KI32_NP = (KI_NP >> np.uint64(29)).astype(np.uint32)
+WI32_NP = (WI_NP * 2.0**29).astype(np.float32)
+
+
+def normals16_from_lcg_words(words: np.ndarray) -> np.ndarray:
+    """One binary16 normal per primary word (fused FP16 / FP16-packed draws)."""
+    w = words.astype(np.uint64)
+    hi = (w >> np.uint64(32)).astype(np.uint32)
+    idx = (hi >> np.uint32(24)).astype(np.int64)
+    sign = ((hi >> np.uint32(23)) & np.uint32(1)).astype(bool)
+    rabs = hi & np.uint32(0x7FFFFF)
+    x = rabs.astype(np.float32) * WI32_NP[idx]  # one binary32 RN multiply
+    x = np.where(sign, -x, x)
+    out = x.astype(np.float16)
+    for i in np.nonzero(~(rabs < KI32_NP[idx]))[0]:
+        out[i] = np.float16(_zig_slow_lcg(int(w[i])))
+    return out
+
+
 class LcgStream:
     """Drop-in `RngStream` replacement (same methods) emitting the LCG stream."""
 

@@ -240,9 +240,22 @@ struct PhxGen {
   }
 };
 
+// One kernel launch as issued by the launch helpers: the per-frame step
+// graph (run_enqueue, F == 1) re-issues a step by updating its kernel nodes
+// with the recorded arguments instead of launching.
+struct LaunchRec {
+  const void* fn;
+  dim3 grid, block;
+  size_t smem;
+  std::vector<unsigned char> args;
+};
+
 // host frames are uploaded in this many chunks on a copy stream; each
 // chunk's likelihood maps start as soon as it lands (pf_run)
 constexpr int kUploadChunks = 8;
+// host frames up to this size are staged through a pinned buffer by the
+// synchronous calls (a per-frame step's frame is 16 KB at 128x128)
+constexpr size_t kStageBytes = 1u << 20;
 
 struct pf_handle {
   int precision = 0, km = 0;
@@ -348,6 +361,22 @@ struct pf_handle {
   // grid dependency wait (likelihood maps, Philox draws): launch it without
   // programmatic overlap
   bool serialize_next = false;
+  // per-frame step graph (F == 1): [frame H2D] -> maps [-> Philox draws] ->
+  // fused -> table, re-launched with updated kernel-node arguments
+  std::vector<LaunchRec>* rec = nullptr;  // launch helpers append here
+  bool rec_only = false;                  // ... and do not launch
+  cudaGraph_t sg = nullptr;
+  cudaGraphExec_t sgx = nullptr;
+  cudaGraphNode_t sg_node[3] = {};  // maps, fused, table
+  int sg_on_dev = -1;
+  const void *sg_frames = nullptr, *sg_maps = nullptr, *sg_traj = nullptr, *sg_noise = nullptr;
+  bool sg_ident = false;
+  // pinned staging of the synchronous calls (pf_run / pf_step)
+  uint8_t* h_stage = nullptr;
+  double* h_traj = nullptr;
+  size_t h_traj_cap = 0;
+  double* traj_user = nullptr;
+  size_t traj_bytes = 0;
   double* noise_all = nullptr;  // [F][K][2]
   size_t noise_cap = 0;
   double* u_all = nullptr;  // [F]
@@ -413,6 +442,12 @@ static cudaError_t set_fused_smem(const pf_handle* h) {
 template <typename Args>
 static cudaError_t launch_pdl(const pf_handle* h, const void* fn, dim3 grid, dim3 block, size_t smem, Args args,
                               bool allow = true) {
+  if (h->rec) {
+    LaunchRec r{fn, grid, block, smem, std::vector<unsigned char>(sizeof(Args))};
+    std::memcpy(r.args.data(), &args, sizeof(Args));
+    h->rec->push_back(std::move(r));
+    if (h->rec_only) return cudaSuccess;
+  }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = grid;
   cfg.blockDim = block;
@@ -482,7 +517,11 @@ int pf_destroy(pf_handle* h) {
       for (int i = 0; i < 8; ++i)
         if (h->peer[sh][i]) cudaIpcCloseMemHandle(h->peer[sh][i]);
   if (h->pending) cudaStreamSynchronize(h->stream);
+  if (h->sgx) cudaGraphExecDestroy(h->sgx);
+  if (h->sg) cudaGraphDestroy(h->sg);
   h->phx.release();
+  if (h->h_stage) cudaFreeHost(h->h_stage);
+  if (h->h_traj) cudaFreeHost(h->h_traj);
   if (h->noise_all) cudaFree(h->noise_all);
   if (h->u_all) cudaFree(h->u_all);
   if (h->xev) cudaEventDestroy(h->xev);
@@ -680,10 +719,21 @@ static int create_impl(pf_handle** out, const pf_config* cfg, int n_shards, int 
   build_exp16(ex.data());
   CK(cudack(cudaMalloc(&h->exp16, 65536 * 2), "exp16"));
   CK(cudack(cudaMemcpy(h->exp16, ex.data(), 65536 * 2, cudaMemcpyHostToDevice), "exp16"));
-  // ziggurat fast-path tables, packed for 16-byte smem staging: 256 x (ki >> 20) then 256 x wi
+  // ziggurat fast-path tables, packed for 16-byte smem staging: 256 x (ki >> 20)
+  // then 256 x wi; binary16 modes: 256 x {ki >> 29, f32(wi * 2^29)} (the
+  // binary32 fast path on the word's high 32 bits, oracle/rng.py)
   {
-    std::vector<unsigned char> zt(pfk::kZigBytes);
+    std::vector<unsigned char> zt(pfk::kZigBytes, 0);
     for (int i = 0; i < 256; ++i) {
+      if (h->km == 2) {
+        double wi;
+        std::memcpy(&wi, &PF_ZIG_WI_BITS_HOST[i], 8);
+        const uint32_t k32 = (uint32_t)(PF_ZIG_KI_HOST[i] >> 29);
+        const float w32 = (float)std::ldexp(wi, 29);  // exact scaling, one RN to binary32
+        std::memcpy(zt.data() + 8 * i, &k32, 4);
+        std::memcpy(zt.data() + 8 * i + 4, &w32, 4);
+        continue;
+      }
       uint32_t khi = (uint32_t)(PF_ZIG_KI_HOST[i] >> 20);
       std::memcpy(zt.data() + 4 * i, &khi, 4);
       std::memcpy(zt.data() + 1024 + 8 * i, &PF_ZIG_WI_BITS_HOST[i], 8);
@@ -899,40 +949,45 @@ static int launch_maps(pf_handle* h, const uint8_t* dframes, int F, int f0 = 0, 
   a.s16 = f64_to_f16(1.0 / std::sqrt(h->params.likelihood_scale * h->n_off));
   a.maps = (char*)h->d_maps + (size_t)f0 * h->Hm * h->Wm * h->rs;
   a.band = h->map_band;
+  // a handful of frames (per-frame steps): narrow bands, so one frame's map
+  // spreads over ~32 CTAs instead of 3-5 long ones (the step's latency)
+  const bool few = h->n_videos * nf < 8;
+  const int few_band = std::max(1, (h->Hm + 31) / 32);
   dim3 grid((h->Hm + a.band - 1) / a.band, h->n_videos * nf);
   if (h->map_runs) {
-    a.band = h->map_runs_band;
+    a.band = few ? std::min(h->map_runs_band, few_band) : h->map_runs_band;
     a.runs = h->d_runs;
     a.n_runs = h->n_runs;
     dim3 gw((h->Hm + a.band - 1) / a.band, h->n_videos * nf);
     // C3, 100 frames: 1.2 ms at 512-1024 threads (1.6 at 256) in both modes
     if (h->km == 0)
-      pfk::pf_map_wide_runs<double><<<gw, 1024, h->map_runs_smem, h->stream>>>(a);
+      PF_CUDA(launch_pdl(h, (const void*)pfk::pf_map_wide_runs<double>, gw, dim3(1024), h->map_runs_smem, a, false), h->err);
     else
-      pfk::pf_map_wide_runs<float><<<gw, 1024, h->map_runs_smem, h->stream>>>(a);
+      PF_CUDA(launch_pdl(h, (const void*)pfk::pf_map_wide_runs<float>, gw, dim3(1024), h->map_runs_smem, a, false), h->err);
   } else if (h->map_wide_img) {
-    a.band = h->map_wide_band;
+    a.band = few ? std::min(h->map_wide_band, few_band) : h->map_wide_band;
     dim3 gw((h->Hm + a.band - 1) / a.band, h->n_videos * nf);
     // measured at C3: FP64 3.3 ms per 100 frames at 1024 threads (6.5 at 256,
     // one CTA per SM either way), FP32 2.0 ms at 256 (2.3 at 1024)
     const int mt = h->km == 0 ? 1024 : pfk::kMapWideThreads;
     if (h->km == 0)
-      pfk::pf_map_wide_img<double><<<gw, mt, h->map_wide_smem, h->stream>>>(a);
+      PF_CUDA(launch_pdl(h, (const void*)pfk::pf_map_wide_img<double>, gw, dim3(mt), h->map_wide_smem, a, false), h->err);
     else
-      pfk::pf_map_wide_img<float><<<gw, mt, h->map_wide_smem, h->stream>>>(a);
+      PF_CUDA(launch_pdl(h, (const void*)pfk::pf_map_wide_img<float>, gw, dim3(mt), h->map_wide_smem, a, false), h->err);
   } else if (h->km == 0)
-    pfk::pf_map_wide<double><<<grid, 256, h->map_smem, h->stream>>>(a);
+    PF_CUDA(launch_pdl(h, (const void*)pfk::pf_map_wide<double>, grid, dim3(256), h->map_smem, a, false), h->err);
   else if (h->km == 1)
-    pfk::pf_map_wide<float><<<grid, 256, h->map_smem, h->stream>>>(a);
+    PF_CUDA(launch_pdl(h, (const void*)pfk::pf_map_wide<float>, grid, dim3(256), h->map_smem, a, false), h->err);
   else if (h->map_img) {
-    const pfk::MapHalfGeom g = pfk::map_half_geom(h->W, h->H, h->r, h->n_off);
+    a.band = few ? few_band : 0;
+    const pfk::MapHalfGeom g = pfk::map_half_geom(h->W, h->H, h->r, h->n_off, a.band);
     dim3 gi((h->Hm + g.band - 1) / g.band, h->n_videos * nf);
     if (h->precision == PF_FP16)  // scalar lanes ("fp16")
-      pfk::pf_map_half_img<false><<<gi, pfk::kMapHalfThreads, g.smem, h->stream>>>(a);
+      PF_CUDA(launch_pdl(h, (const void*)pfk::pf_map_half_img<false>, gi, dim3(pfk::kMapHalfThreads), g.smem, a, false), h->err);
     else
-      pfk::pf_map_half_img<true><<<gi, pfk::kMapHalfThreads, g.smem, h->stream>>>(a);
+      PF_CUDA(launch_pdl(h, (const void*)pfk::pf_map_half_img<true>, gi, dim3(pfk::kMapHalfThreads), g.smem, a, false), h->err);
   } else
-    pfk::pf_map_half<<<grid, 256, h->map_smem, h->stream>>>(a);
+    PF_CUDA(launch_pdl(h, (const void*)pfk::pf_map_half, grid, dim3(256), h->map_smem, a, false), h->err);
   h->launches += 1;
   h->serialize_next = true;
   PF_CUDA(cudaGetLastError(), h->err);
@@ -940,6 +995,8 @@ static int launch_maps(pf_handle* h, const uint8_t* dframes, int F, int f0 = 0, 
 }
 
 static int shard_tables_launch(pf_handle* h, int traj_index, int traj_stride);
+static int launch_frame(pf_handle* h, const void* map_slot, long long map_video_stride, int traj_index,
+                        int traj_stride);
 
 // one frame: fused kernel + tile table
 static int launch_frame(pf_handle* h, const void* map_slot, long long map_video_stride, int traj_index,
@@ -1089,8 +1146,107 @@ static int finish_degenerate(pf_handle* h) {  // after the stream is synchronise
 // Enqueue a whole-video run on the handle's stream, ordered after `ext`'s
 // prior work when ext is given (and `ext` ordered after the run); no host
 // synchronisation.  run_complete() waits and reads the timings / degeneracy.
+// pageable host memory?  (the synchronous calls stage small copies through
+// pinned buffers: a pageable cudaMemcpyAsync is a blocking, driver-staged copy)
+static bool is_pageable(const void* p) {
+  cudaPointerAttributes at{};
+  if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+    cudaGetLastError();
+    return true;
+  }
+  return at.type == cudaMemoryTypeUnregistered;
+}
+
+// One per-frame step (F == 1) as ONE graph launch: [frame H2D from the pinned
+// staging buffer] -> maps [-> Philox draws] -> fused -> table, captured once;
+// later steps re-record the three kernels' arguments (frame counter, jump
+// constants, buffer parity, frame pointer) without launching and update the
+// graph's kernel nodes.  Same kernels, same arguments: same results.
+static int step_graph_launch(pf_handle* h, const uint8_t* dframes, int on_device) {
+  const size_t map_elems = (size_t)h->Hm * h->Wm;
+  const void* frames_key = on_device ? nullptr : (const void*)h->d_frames;
+  const bool rebuild = !h->sgx || h->sg_on_dev != on_device || h->sg_maps != h->d_maps || h->sg_traj != h->d_traj ||
+                       h->sg_noise != (const void*)h->noise_all || h->sg_frames != frames_key;
+  std::vector<LaunchRec> recs;
+  int rc;
+  if (rebuild) {
+    if (h->sgx) cudaGraphExecDestroy(h->sgx);
+    if (h->sg) cudaGraphDestroy(h->sg);
+    h->sgx = nullptr;
+    h->sg = nullptr;
+    if (h->philox && (rc = h->phx.reserve(2 * h->K, h->err))) return rc;  // no allocation while capturing
+    h->rec = &recs;
+    h->rec_only = false;
+    PF_CUDA(cudaStreamBeginCapture(h->stream, cudaStreamCaptureModeThreadLocal), h->err);
+    auto fail = [&](int code) {
+      h->rec = nullptr;
+      cudaGraph_t g = nullptr;
+      cudaStreamEndCapture(h->stream, &g);
+      if (g) cudaGraphDestroy(g);
+      return code;
+    };
+    if (!on_device && cudaMemcpyAsync(h->d_frames, h->h_stage, (size_t)h->n_videos * h->H * h->W,
+                                      cudaMemcpyHostToDevice, h->stream) != cudaSuccess)
+      return fail(PF_ECUDA);
+    if ((rc = launch_maps(h, dframes, 1))) return fail(rc);
+    if (h->philox && (rc = h->phx.draw(h->stream, 2 * h->K, h->noise_all, h->u_all, h->err))) return fail(rc);
+    if ((rc = launch_frame(h, h->d_maps, (long long)map_elems, 0, 1))) return fail(rc);
+    h->rec = nullptr;
+    PF_CUDA(cudaStreamEndCapture(h->stream, &h->sg), h->err);
+    PF_CUDA(cudaGraphInstantiate(&h->sgx, h->sg, 0), h->err);
+    if (recs.size() != 3) {
+      h->err = "step graph: unexpected launch sequence";
+      return PF_ECUDA;
+    }
+    size_t n = 0;
+    PF_CUDA(cudaGraphGetNodes(h->sg, nullptr, &n), h->err);
+    std::vector<cudaGraphNode_t> nodes(n);
+    PF_CUDA(cudaGraphGetNodes(h->sg, nodes.data(), &n), h->err);
+    for (auto& nd : h->sg_node) nd = nullptr;
+    for (cudaGraphNode_t nd : nodes) {
+      cudaGraphNodeType ty;
+      PF_CUDA(cudaGraphNodeGetType(nd, &ty), h->err);
+      if (ty != cudaGraphNodeTypeKernel) continue;
+      cudaKernelNodeParams kp{};
+      PF_CUDA(cudaGraphKernelNodeGetParams(nd, &kp), h->err);
+      for (int i = 0; i < 3; ++i)
+        if (kp.func == recs[i].fn) h->sg_node[i] = nd;
+    }
+    if (!h->sg_node[0] || !h->sg_node[1] || !h->sg_node[2]) {
+      h->err = "step graph: kernel nodes not found";
+      return PF_ECUDA;
+    }
+    h->sg_on_dev = on_device;
+    h->sg_maps = h->d_maps;
+    h->sg_traj = h->d_traj;
+    h->sg_noise = h->noise_all;
+    h->sg_frames = frames_key;
+  } else {
+    h->rec = &recs;
+    h->rec_only = true;  // arguments only (the Philox draws' arguments never change)
+    rc = launch_maps(h, dframes, 1);
+    if (!rc) rc = launch_frame(h, h->d_maps, (long long)map_elems, 0, 1);
+    h->rec = nullptr;
+    h->rec_only = false;
+    if (rc) return rc;
+    for (int i = 0; i < 3; ++i) {
+      cudaKernelNodeParams kp{};
+      kp.func = const_cast<void*>(recs[i].fn);
+      kp.gridDim = recs[i].grid;
+      kp.blockDim = recs[i].block;
+      kp.sharedMemBytes = (unsigned)recs[i].smem;
+      void* args[1] = {recs[i].args.data()};
+      kp.kernelParams = args;
+      PF_CUDA(cudaGraphExecKernelNodeSetParams(h->sgx, h->sg_node[i], &kp), h->err);
+    }
+  }
+  PF_CUDA(cudaGraphLaunch(h->sgx, h->stream), h->err);
+  if (h->philox) h->launches += 4;
+  return PF_OK;
+}
+
 static int run_enqueue(pf_handle* h, const uint8_t* frames, int32_t F, int32_t on_device, double* traj_out,
-                       cudaStream_t ext) {
+                       cudaStream_t ext, bool sync_call = false) {
   if (!h || !frames || F < 1 || !traj_out) return PF_EINVAL;
   if (h->n_shards > 1) {
     h->err = "sharded handle: drive frames with pf_shard_*";
@@ -1130,6 +1286,23 @@ static int run_enqueue(pf_handle* h, const uint8_t* frames, int32_t F, int32_t o
     dframes = h->d_frames;
   }
   PF_CUDA(cudaEventRecord(h->ev[0], h->stream), h->err);
+  // per-frame steps: one graph launch (stage timings collapse to "frames")
+  const bool step_graph = F == 1 && h->use_graphs && !h->profiling && !h->tracing && !h->dbg_anc &&
+                          !h->split_table && (on_device || (sync_call && fbytes <= kStageBytes));
+  if (step_graph) {
+    if (!on_device) {
+      if (!h->h_stage) PF_CUDA(cudaMallocHost(&h->h_stage, kStageBytes), h->err);
+      PF_CUDA(cudaStreamSynchronize(h->stream), h->err);  // the staging buffer's previous copy is done
+      std::memcpy(h->h_stage, frames, fbytes);
+    }
+    if (h->philox) {
+      if ((rc = grow((void**)&h->noise_all, &h->noise_cap, (size_t)2 * h->K * 8, h->err))) return rc;
+      if ((rc = grow((void**)&h->u_all, &h->u_cap, 8, h->err))) return rc;
+    }
+    PF_CUDA(cudaEventRecord(h->ev[1], h->stream), h->err);
+    PF_CUDA(cudaEventRecord(h->ev[2], h->stream), h->err);
+    if ((rc = step_graph_launch(h, dframes, on_device))) return rc;
+  } else {
   // (C3's 100 MB: 31.4 -> 30.0 ms per step; below ~8 MB the extra map launches
   // cost more than the upload they hide -- C2's 1.6 MB: +0.1 ms)
   if (!on_device && h->n_videos == 1 && F >= kUploadChunks && fbytes >= (8u << 20)) {
@@ -1155,8 +1328,16 @@ static int run_enqueue(pf_handle* h, const uint8_t* frames, int32_t F, int32_t o
       if ((rc = launch_maps(h, dframes, F, f0, nf))) return rc;
     }
   } else {
-    if (!on_device)
-      PF_CUDA(cudaMemcpyAsync(h->d_frames, frames, fbytes, cudaMemcpyHostToDevice, h->stream), h->err);
+    if (!on_device) {
+      const uint8_t* src = frames;
+      if (sync_call && fbytes <= kStageBytes && is_pageable(frames)) {  // small host frames: pinned staging
+        if (!h->h_stage) PF_CUDA(cudaMallocHost(&h->h_stage, kStageBytes), h->err);
+        PF_CUDA(cudaStreamSynchronize(h->stream), h->err);  // the staging buffer's previous copy is done
+        std::memcpy(h->h_stage, frames, fbytes);
+        src = h->h_stage;
+      }
+      PF_CUDA(cudaMemcpyAsync(h->d_frames, src, fbytes, cudaMemcpyHostToDevice, h->stream), h->err);
+    }
     PF_CUDA(cudaEventRecord(h->ev[1], h->stream), h->err);
     if ((rc = launch_maps(h, dframes, F))) return rc;
   }
@@ -1212,10 +1393,26 @@ static int run_enqueue(pf_handle* h, const uint8_t* frames, int32_t F, int32_t o
       if ((rc = launch_frame(h, slot, vstride, f, F))) return rc;
     }
   }
+  }  // not a step graph
   PF_CUDA(cudaEventRecord(h->ev[3], h->stream), h->err);
-  // device or (pinned / pageable) host destination
-  PF_CUDA(cudaMemcpyAsync(traj_out, h->d_traj, (size_t)h->n_tracks * F * 2 * 8, cudaMemcpyDefault, h->stream),
-          h->err);
+  // device or (pinned / pageable) host destination; a synchronous call with a
+  // pageable destination lands in pinned memory and is copied out after the sync
+  const size_t tbytes = (size_t)h->n_tracks * F * 2 * 8;
+  h->traj_user = nullptr;
+  if (sync_call && is_pageable(traj_out)) {
+    if (h->h_traj_cap < tbytes) {
+      if (h->h_traj) cudaFreeHost(h->h_traj);
+      h->h_traj = nullptr;
+      h->h_traj_cap = 0;
+      PF_CUDA(cudaMallocHost(&h->h_traj, tbytes), h->err);
+      h->h_traj_cap = tbytes;
+    }
+    PF_CUDA(cudaMemcpyAsync(h->h_traj, h->d_traj, tbytes, cudaMemcpyDeviceToHost, h->stream), h->err);
+    h->traj_user = traj_out;
+    h->traj_bytes = tbytes;
+  } else {
+    PF_CUDA(cudaMemcpyAsync(traj_out, h->d_traj, tbytes, cudaMemcpyDefault, h->stream), h->err);
+  }
   if ((rc = queue_degenerate(h))) return rc;
   PF_CUDA(cudaEventRecord(h->ev[4], h->stream), h->err);
   if (ext) {  // the caller's later work sees the trajectory
@@ -1234,6 +1431,10 @@ static int run_complete(pf_handle* h) {
   PF_CUDA(cudaStreamSynchronize(h->stream), h->err);
   h->pending = false;
   const int F = h->pending_F;
+  if (h->traj_user) {
+    std::memcpy(h->traj_user, h->h_traj, h->traj_bytes);
+    h->traj_user = nullptr;
+  }
   if (h->philox) {
     const int rc = h->phx.check(h->err);
     if (rc) return rc;
@@ -1265,7 +1466,7 @@ static int run_complete(pf_handle* h) {
 }
 
 int pf_run(pf_handle* h, const uint8_t* frames, int32_t F, int32_t on_device, double* traj_out) {
-  int rc = run_enqueue(h, frames, F, on_device, traj_out, nullptr);
+  int rc = run_enqueue(h, frames, F, on_device, traj_out, nullptr, true);
   if (rc) return rc;
   return run_complete(h);
 }

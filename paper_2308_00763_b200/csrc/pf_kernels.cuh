@@ -482,10 +482,12 @@ struct MapHalfGeom {
   int band, P, rows_img;  // map rows per CTA, image pitch (halves, even), image rows
   size_t smem;            // dynamic shared memory bytes
 };
-__host__ __device__ inline MapHalfGeom map_half_geom(int W, int H, int r, int n_off) {
+// band_cap > 0 limits the map rows per CTA (few frames: more, shorter CTAs)
+__host__ __device__ inline MapHalfGeom map_half_geom(int W, int H, int r, int n_off, int band_cap = 0) {
   MapHalfGeom g;
   const int Wm = W + 2 * r, Hm = H + 2 * r, npr = (Wm + 1) / 2;
   g.band = max(1, min(Hm, kMapHalfThreads * kMapHalfPairs / npr));
+  if (band_cap > 0) g.band = min(g.band, band_cap);
   g.P = (Wm + 2 * r + 2) & ~1;
   g.rows_img = g.band + 2 * r;
   const size_t frame_rows = (size_t)(g.band + 2 * r) * W + 32;
@@ -496,7 +498,7 @@ __host__ __device__ inline MapHalfGeom map_half_geom(int W, int H, int r, int n_
 template <bool PK>  // PK: one HADD2 per entry pair and tap; else two scalar HADDs (same values)
 __global__ void __launch_bounds__(kMapHalfThreads) pf_map_half_img(MapArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
-  const MapHalfGeom g = map_half_geom(a.W, a.H, a.r, a.n_off);
+  const MapHalfGeom g = map_half_geom(a.W, a.H, a.r, a.n_off, a.band);
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem);
   __half* term = reinterpret_cast<__half*>(smem + 16);
   int* tapw = reinterpret_cast<int*>(smem + 16 + 512);
@@ -973,6 +975,7 @@ constexpr int max_src_tiles() {  // source tiles staged in shared memory (else g
 // it copies every source position, not only the ancestors; not done)
 
 // ziggurat fast-path tables in shared memory: 256 x (ki >> 20) then 256 x wi
+// (FP64 / FP32); binary16 modes: 256 x {ki >> 29, f32(wi * 2^29)} (2 KB)
 // (a 512-entry signed {wi, ki} table was measured: fewer instructions, but the
 // 8 KB per-CTA staging and 16-byte random reads made C2 / C3 slower)
 constexpr int kZigBytes = 3072;
@@ -1073,10 +1076,13 @@ __device__ __forceinline__ double tree_vpt(const double* v) {
 // 5.64e10, FP32 6 (40 registers) 4.30 -> 4.45e10; FP64 5 (48 registers; 40
 // lose 3%); the 128-thread variants keep the compiler's choice (C2 FP16 at 40
 // registers: -9%).
+#ifndef PF_MINB_FP16_256
+#define PF_MINB_FP16_256 7  // A/B knob (make EXTRA=-DPF_MINB_FP16_256=6)
+#endif
 template <int MODE>
 constexpr int fused_min_blocks(int tpb) {
   return tpb == 128 ? (MODE == M_FP32 ? 7 : MODE == M_FP64 ? 6 : 0)
-         : tpb != 256 ? 0 : MODE == M_FP16 ? 7 : MODE == M_FP32 ? 6 : 4;  // 0: no constraint
+         : tpb != 256 ? 0 : MODE == M_FP16 ? PF_MINB_FP16_256 : MODE == M_FP32 ? 6 : 4;  // 0: no constraint
 }
 
 // One CTA = one tile of PF_TILE particles of one track; TPB = PF_TILE/(VPT*R)
@@ -1101,6 +1107,7 @@ __global__ void __launch_bounds__(PF_TILE / (VPT * R), fused_min_blocks<MODE>(PF
   extern __shared__ __align__(16) unsigned char smem[];
   const uint32_t* s_kihi = reinterpret_cast<const uint32_t*>(smem);    // 1 KB
   const double* s_wi = reinterpret_cast<const double*>(smem + 1024);  // 2 KB
+  const uint2* s_kw32 = reinterpret_cast<const uint2*>(smem);         // FP16: {ki32, wi32 bits} x 256
   vec* s_X = reinterpret_cast<vec*>(smem + kZigBytes);                // per-particle scaled noise
   real* s_c = reinterpret_cast<real*>(smem + kZigBytes + PF_TILE * sizeof(vec));
   unsigned char* p_tab = reinterpret_cast<unsigned char*>(s_c + MS * PF_TILE);
@@ -1220,6 +1227,29 @@ __global__ void __launch_bounds__(PF_TILE / (VPT * R), fused_min_blocks<MODE>(PF
     unsigned slow = 0;  // bit 2i+c: normal (i, c) needs the slow path
 #pragma unroll
     for (int i = 0; i < VPT; ++i) {
+      if constexpr (MODE == M_FP16) {
+        // binary16 modes: precision-matched draws (oracle/rng.py
+        // normals16_from_lcg_words): the same words, fast path in binary32 on
+        // the high 32 bits -- idx = bits 56..63, sign = bit 55, rabs = bits
+        // 32..54 -- x = RN32(rabs * wi32[idx]), accepted iff rabs < ki32[idx]
+        // ({ki32, wi32} per layer in one 8-byte shared entry), then RN16
+        float nf[2];
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+          const unsigned whi = (unsigned)(xs >> 32);
+          xs = pfr::kA * xs + pfr::kC;
+          const unsigned rabs = whi & 0x7fffffu;
+          const uint2 kw = s_kw32[whi >> 24];
+          const float x = __fmul_rn(__fsub_rn(__uint_as_float(0x4b000000u | rabs), 8388608.0f), __uint_as_float(kw.y));
+          nf[c] = __uint_as_float(__float_as_uint(x) ^ ((whi << 8) & 0x80000000u));
+          slow |= (rabs >= kw.x ? 1u : 0u) << (2 * i + c);
+        }
+        const __half2 nh = __floats2half2_rn(nf[0], nf[1]);
+        if constexpr (!PK)
+          s_X[l0 + i] = scale_noise_scalar(nh, stdv);
+        else
+          s_X[l0 + i] = __hmul2_rn(stdv, nh);
+      } else {
       double nn[2];
 #pragma unroll
       for (int c = 0; c < 2; ++c) {
@@ -1237,10 +1267,8 @@ __global__ void __launch_bounds__(PF_TILE / (VPT * R), fused_min_blocks<MODE>(PF
         // fast-path test rabs < ki on the top 32 bits of rabs (bits 23..54 of w)
         slow |= (__funnelshift_r(wlo, whi, 23) >= s_kihi[idx] ? 1u : 0u) << (2 * i + c);
       }
-      if constexpr (MODE == M_FP16 && !PK)
-        s_X[l0 + i] = scale_noise_scalar(to_vec<MODE>(nn[0], nn[1]), stdv);
-      else
-        s_X[l0 + i] = scale_noise<MODE>(to_vec<MODE>(nn[0], nn[1]), stdv);
+      s_X[l0 + i] = scale_noise<MODE>(to_vec<MODE>(nn[0], nn[1]), stdv);
+      }  // FP64 / FP32 draws
     }
     if (l0 + VPT > Tb) slow = l0 >= Tb ? 0u : slow & ((1u << (2 * (Tb - l0))) - 1u);
     while (slow) {  // rare per thread: re-derive the word by stepping from xs0

@@ -66,12 +66,21 @@ def main():
         enq(t)
     L.pf_sync(f._h)
     f.reset()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     t0 = time.perf_counter()
+    e0.record()
     for t in range(args.n):
         enq(t)
+    t1 = time.perf_counter()
+    e1.record()
     L.pf_sync(f._h)
     torch.cuda.synchronize()
-    print(f"{'pf_step_async pipelined (device frames)':40s} {1e6 * (time.perf_counter() - t0) / args.n:8.1f} us/frame")
+    t2 = time.perf_counter()
+    print(f"{'pf_step_async pipelined (device frames)':40s} {1e6 * (t2 - t0) / args.n:8.1f} us/frame  "
+          f"(host enqueue {1e6 * (t1 - t0) / args.n:.1f} us/frame, device {1e3 * e0.elapsed_time(e1) / args.n:.1f} "
+          f"us/frame)")
+    f.reset()
     ref = f.run(host)
     print("pipelined steps == run():", bool(np.array_equal(outs.cpu().numpy(), ref)))
 
