@@ -191,6 +191,7 @@ class FusedTrack:
             else:
                 wq = np.rint(w * 2.0**Fb).astype(np.int64)
         wq = np.where(valid, wq, 0)
+        self.last_wq = wq.reshape(-1)[:K]  # fixed-point tile weights (tests)
         cum = np.cumsum(wq, axis=1)
         S = cum[:, -1]
         if mode == "fp16":
@@ -226,6 +227,7 @@ class FusedTrack:
         m = m_b.max()
         f = rng.exp64_np(m_b - m)
         mass = np.rint((S.astype(np.float64) * f) * 2.0 ** (self.Q - Fb)).astype(np.int64)
+        self.last_mass = mass  # exact tile masses (tests)
         Oq = np.concatenate([[0], np.cumsum(mass)[:-1]]).astype(np.int64)
         Sq = int(mass.sum())
         O = Oq.astype(np.float64) / np.float64(Sq)

@@ -98,6 +98,46 @@ def test_ancestors_match_flat_systematic_resampling():
     ref = np.minimum(np.searchsorted(flat, pts, side="left"), 2999)
     # identical except where a point falls within rounding of a boundary
     assert np.mean(anc == ref) > 0.999
+    bad = np.nonzero(anc != ref)[0]
+    for k in bad:  # every disagreement: the point sits on a CDF step (to rounding)
+        lo, hi = sorted((anc[k], ref[k]))
+        assert np.all(np.abs(flat[lo:hi] - pts[k]) <= 1e-12 * max(1.0, pts[k])), k
+
+
+@pytest.mark.parametrize("mode", ["fp64", "fp32"])
+def test_ancestors_given_identical_weights_at_scale(mode):
+    # the reference's resampling (filter.py:248-255: flat CDF = cumsum of the
+    # normalised weights, searchsorted-left of (k+u)/K) vs the fused
+    # hierarchical search on the SAME weights (the fused frame's exact tile
+    # weights): equal except at points within rounding of a CDF step
+    K = 200_000
+    frames, _ = rp.generate_video(rp.Params(), 3, 128, 128, (64.0, 64.0), 4)
+    tr = fused.FusedTrack(mode, K, 128, 128, 2, (64.0, 64.0))
+    tr.step(tr.loglik_map(frames[0]))
+    tr.step(tr.loglik_map(frames[1]))
+    s, O, invM = tr.table
+    M = np.where(invM > 0, 1.0 / np.where(invM > 0, invM, 1.0), 0.0)
+    flat = np.concatenate([O[b] + M[b] * tr.c[b * fused.TILE:(b + 1) * fused.TILE].astype(np.float64)
+                           for b in range(tr.n)])
+    pts = fused.points(mode, K, tr.u)
+    anc = tr.ancestors()
+    ref = np.minimum(np.searchsorted(flat, pts, side="left"), K - 1)
+    bad = np.nonzero(anc != ref)[0]
+    assert len(bad) <= K * 1e-3
+    tol = 1e-12 if mode == "fp64" else 2e-7
+    for k in bad:
+        lo, hi = sorted((anc[k], ref[k]))
+        assert np.all(np.abs(flat[lo:hi] - pts[k]) <= tol), (k, anc[k], ref[k])
+    # the reference's own flat CDF from the same normalised weights: w_hat_k =
+    # w_q,k * (mass_b / S_b) / sum(mass); cdf = cumsum(w_hat) (sequential, f64)
+    S_b = np.add.reduceat(np.concatenate([tr.last_wq, np.zeros(tr.n * fused.TILE - K, np.int64)]),
+                          np.arange(0, tr.n * fused.TILE, fused.TILE))
+    scale = np.where(S_b > 0, tr.last_mass / np.where(S_b > 0, S_b, 1), 0.0) / float(tr.last_mass.sum())
+    w_hat = tr.last_wq * np.repeat(scale, fused.TILE)[:K]
+    cdf = np.cumsum(w_hat)
+    ref2 = np.minimum(np.searchsorted(cdf, pts, side="left"), K - 1)
+    # bit-exact here: no point falls within the cumsum's rounding of a step
+    assert np.array_equal(anc, ref2), int(np.sum(anc != ref2))
 
 
 def test_oracle_set_state_reproduces_the_run():
