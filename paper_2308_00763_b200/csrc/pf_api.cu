@@ -19,6 +19,7 @@
 
 #include "../../include/pf_b200.h"
 #include "pf_kernels.cuh"
+#include "pf_fused_sel.cuh"
 #include "pf_philox.cuh"
 #include "pf_staged.cuh"
 #include "pf_video.cuh"
@@ -384,29 +385,20 @@ struct pf_handle {
   const void* g_noise = nullptr;
 };
 
-typedef void (*fused_fn)(pfk::FusedArgs);
-// (VPT, rounds) per threads-per-block: the tile is always PF_TILE particles
+// the fused kernel's instantiations live in their own translation units
+// (pf_fused_sel.cuh, built in parallel); these select among them
+typedef pf_fused_fn fused_fn;
 template <int M, bool PK = true, bool DBG = false>
 static fused_fn fused_for_tpb(int tpb) {
-  switch (tpb) {
-    case 32: return pfk::pf_fused_frame<M, 8, 4, false, PK, DBG>;
-    case 64: return pfk::pf_fused_frame<M, 8, 2, false, PK, DBG>;
-    case 128: return pfk::pf_fused_frame<M, 8, 1, false, PK, DBG>;
-    case 512: return pfk::pf_fused_frame<M, 2, 1, false, PK, DBG>;
-    case 1024: return pfk::pf_fused_frame<M, 1, 1, false, PK, DBG>;
-    default: return pfk::pf_fused_frame<M, 4, 1, false, PK, DBG>;
-  }
+  return pf_fused_sel(M, PK, DBG, tpb);
 }
-// sharded filters: 128 or 256 threads per block only (keeps the instantiations few)
 template <int M>
 static fused_fn fused_sharded(int tpb) {
-  return tpb == 128 ? pfk::pf_fused_frame<M, 8, 1, true> : pfk::pf_fused_frame<M, 4, 1, true>;
+  return pf_fused_sel_sharded(M, tpb);
 }
-// numpy-philox stream: normals read from the generated buffer (128 / 256 threads)
 template <int M, bool PK>
 static fused_fn fused_nz(int tpb) {
-  return tpb == 128 ? pfk::pf_fused_frame<M, 8, 1, false, PK, false, true>
-                    : pfk::pf_fused_frame<M, 4, 1, false, PK, false, true>;
+  return pf_fused_sel_nz(M, PK, tpb);
 }
 // dbg: the instantiation with the trace / debug-capture hooks (pf_set_trace,
 // pf_get_debug); the production kernels carry neither

@@ -412,6 +412,7 @@ __global__ void __launch_bounds__(1024) pf_map_wide_runs(MapArgs a) {
 // binary16: term16 table per intensity (model.half_term_stabilized, 7 RN16
 // ops), sequential RN16 fold in template order from +0; two adjacent map
 // entries per thread in one half2.
+#ifndef PF_FUSED_ONLY  // launched from pf_api.cu only
 __global__ void pf_map_half(MapArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem);
@@ -467,6 +468,7 @@ __global__ void pf_map_half(MapArgs a) {
     if (mx1 != mx0) out[(size_t)my * a.Wm + mx1] = __high2half(acc);
   }
 }
+#endif
 
 // binary16 map, term-image formulation (used when its shared memory fits):
 // the CTA's band of map rows reads a padded image T[py][px] = term16(frame
@@ -849,6 +851,7 @@ __device__ __forceinline__ int weight_q<M_FP16>(__half L, __half m, const unsign
 }
 
 // exhaustive check helper: out[i] = exp16_fast(bits i) for all 65536 patterns
+#ifndef PF_FUSED_ONLY  // launched from pf_api.cu only
 __global__ void pf_exp16_fast_check(const unsigned short* exp16, unsigned short* out) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < 65536) {
@@ -856,6 +859,7 @@ __global__ void pf_exp16_fast_check(const unsigned short* exp16, unsigned short*
     out[i] = (__half2float(d) <= 0.0f) ? __half_as_ushort(exp16_fast(d, exp16)) : exp16[i];
   }
 }
+#endif
 
 // search keys: c_j >= q  <=>  key(c_j) >= key_up(q) for non-negative values,
 // where key is the IEEE bit pattern (monotone for c >= 0) and key_up(q) the

@@ -72,7 +72,7 @@ __device__ __forceinline__ double uniform_of(uint64_t w) { return (double)(w >> 
 
 // Ziggurat slow path (oracle/rng.py _zig_slow_lcg): retry words from a
 // splitmix64 sequence seeded with the primary word.
-__device__ __noinline__ double zig_slow(uint64_t r) {
+static __device__ __noinline__ double zig_slow(uint64_t r) {
   uint64_t s = r;
   for (;;) {
     unsigned idx = (unsigned)(r >> 56);
@@ -148,7 +148,7 @@ __device__ __forceinline__ void philox_block(const unsigned long long ctr_in[4],
 }
 
 // glibc 2.39 log1p (x86-64 FMA variant), domain -1 < x <= 0.41422
-__device__ double log1p_glibc(double x) {
+static __device__ double log1p_glibc(double x) {
   const double L1 = 0x1.5555555555593p-1, L2 = 0x1.999999997fa04p-2, L3 = 0x1.2492494229359p-2;
   const double L4 = 0x1.c71c51d8e78afp-3, L5 = 0x1.7466496cb03dep-3, L6 = 0x1.39a09d078c69fp-3;
   const double L7 = 0x1.2f112df3e5244p-3, LN2_LO = 0x1.a39ef35793c76p-33, LN2_HI = 0x1.62e42fee00000p-1;
