@@ -315,7 +315,7 @@ struct pf_handle {
   float timings[6] = {0};
   int64_t launches = 0;
   int degenerate_frame = -1;
-  size_t map_smem = 0, fused_smem = 0;
+  size_t map_smem = 0, fused_smem = 0, fused_smem_base = 0;
   int map_band = 32;
   bool map_wide_img = false;  // FP32 / FP64 term-image map kernel
   int map_wide_band = 8;
@@ -419,9 +419,29 @@ static fused_fn fused_kernel(const pf_handle* h, int dbg = -1) {
   const bool d = dbg < 0 ? fused_dbg(h) : dbg != 0;
   return d ? fused_unsharded<true>(h) : fused_unsharded<false>(h);
 }
-static cudaError_t set_fused_smem(const pf_handle* h) {
-  cudaError_t e = cudaFuncSetAttribute((const void*)fused_kernel(h, 0), cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)h->fused_smem);
+// Dynamic shared memory of the fused launches.  When a frame's whole grid is
+// one wave (C1 / C2 sizes), the footprint is padded so that no SM holds more
+// than ceil(CTAs / SMs) of them: the block scheduler otherwise packs up to the
+// occupancy limit on some SMs (e.g. 10 FP16 CTAs where 6.6 is the mean), and
+// the frame waits for the most loaded SM (C2 FP16 +7%, same-box A/B).
+static cudaError_t set_fused_smem(pf_handle* h) {
+  h->fused_smem = h->fused_smem_base;
+  int cap = 0;
+  if (const char* mb = std::getenv("PF_FUSED_MAXB")) cap = std::atoi(mb);  // A/B knob (0: no padding)
+  int per_sm = 0, sms = 0, sm_smem = 0, resv = 0;
+  const void* k0 = (const void*)fused_kernel(h, 0);
+  cudaError_t e = cudaFuncSetAttribute(k0, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->fused_smem);
+  if (e == cudaSuccess && h->n_shards == 1 && (cap > 0 || std::getenv("PF_FUSED_MAXB") == nullptr) &&
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, h->device) == cudaSuccess &&
+      cudaDeviceGetAttribute(&sm_smem, cudaDevAttrMaxSharedMemoryPerMultiprocessor, h->device) == cudaSuccess &&
+      cudaDeviceGetAttribute(&resv, cudaDevAttrReservedSharedMemoryPerBlock, h->device) == cudaSuccess &&
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k0, h->tpb, h->fused_smem) == cudaSuccess) {
+    const long long total = (long long)h->nl * h->n_tracks;
+    if (cap <= 0 && total <= (long long)per_sm * sms) cap = (int)((total + sms - 1) / sms);
+    if (cap > 0 && cap < per_sm) h->fused_smem = std::max(h->fused_smem, (size_t)(sm_smem / (cap + 1) - resv + 16));
+  }
+  cudaGetLastError();
+  e = cudaFuncSetAttribute(k0, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->fused_smem);
   if (e == cudaSuccess && h->n_shards == 1 && !h->philox)
     e = cudaFuncSetAttribute((const void*)fused_kernel(h, 1), cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)h->fused_smem);
@@ -754,8 +774,8 @@ static int create_impl(pf_handle** out, const pf_config* cfg, int n_shards, int 
   size_t rows_bytes = (size_t)(h->map_band + 2 * h->r) * h->W + 32;
   h->map_smem = 16 + 256 * h->rs + h->n_off * sizeof(int2) + h->n_plan * (sizeof(short) + sizeof(short2)) + 16 +
                 rows_bytes;
-  h->fused_smem = h->km == 0 ? pfk::fused_smem_bytes<0>() : h->km == 1 ? pfk::fused_smem_bytes<1>()
-                                                                      : pfk::fused_smem_bytes<2>();
+  h->fused_smem_base = h->km == 0 ? pfk::fused_smem_bytes<0>() : h->km == 1 ? pfk::fused_smem_bytes<1>()
+                                                                           : pfk::fused_smem_bytes<2>();
   CK(cudack(set_fused_smem(h), "fused smem attr"));
   // binary16: the term-image kernel when its shared memory fits
   h->map_img = false;
