@@ -74,6 +74,25 @@ __device__ __forceinline__ __half hadd_s(__half a, __half b) {
 __device__ __forceinline__ __half hmul_s(__half a, __half b) {
   return __float2half_rn(__fmul_rn(__half2float(a), __half2float(b)));
 }
+__device__ __forceinline__ __half hsub_s(__half a, __half b) {
+  return __float2half_rn(__fsub_rn(__half2float(a), __half2float(b)));
+}
+// The naive kernel's per-particle re-derivation of shared constants (the
+// reference's naive FP16 path, filter.py:482-490,535-541, and the paper's
+// un-optimised resampling kernel): casts and reciprocals are
+// issued for every particle instead of once per tile.  `asm volatile` keeps
+// the compiler from hoisting them; the values are those of the hoisted forms.
+__device__ __forceinline__ float cvt_f32_f64_naive(double d) {
+  float f;
+  asm volatile("cvt.rn.f32.f64 %0, %1;" : "=f"(f) : "d"(d));
+  return f;
+}
+__device__ __forceinline__ float rcp_f32_s64_naive(long long S) {
+  float s, r;
+  asm volatile("cvt.rn.f32.s64 %0, %1;" : "=f"(s) : "l"(S));
+  asm volatile("div.rn.f32 %0, 0f3F800000, %1;" : "=f"(r) : "f"(s));
+  return r;
+}
 // ------------------------------------------------------------------------
 // TMA bulk copy helpers (cp.async.bulk + mbarrier)
 // ------------------------------------------------------------------------
@@ -1499,7 +1518,11 @@ __global__ void __launch_bounds__(PF_TILE / (VPT * R), fused_min_blocks<MODE>(PF
             typename KT::k_t kq;
             if constexpr (MODE == M_FP16) {
               // f32 tile-local point: q = ((k - s_b) + phi_b) * rho_b
-              const float qf = __fmul_rn(__fadd_rn((float)(k - sb), fO), fM);
+              float qf;
+              if constexpr (PK)
+                qf = __fmul_rn(__fadd_rn((float)(k - sb), fO), fM);
+              else  // naive: the tile's f32 offset and scale re-cast from f64 for every particle
+                qf = __fmul_rn(__fadd_rn((float)(k - sb), cvt_f32_f64_naive(gO)), cvt_f32_f64_naive(gM));
               kq = __half_as_ushort(__float2half_ru(fminf(fmaxf(qf, 0.0f), 1.0f)));
             } else {
               const double p = point_of<MODE>(k, u, K, invK);
@@ -1615,7 +1638,13 @@ __global__ void __launch_bounds__(PF_TILE / (VPT * R), fused_min_blocks<MODE>(PF
     double px[VPT], py[VPT];
 #pragma unroll
     for (int i = 0; i < VPT; ++i) {
-      const wq_t w = weight_q<MODE>(Lr[rr][i], mtile, a.exp16);  // 0 outside the tile (L = -inf)
+      wq_t w;  // 0 outside the tile (L = -inf)
+      if constexpr (MODE == M_FP16 && !PK) {  // naive: per-op f32 round trips (same values)
+        const __half d = hsub_s(Lr[rr][i], mtile);
+        w = __float2int_rn(__fmul_rn(__half2float(__ushort_as_half(__ldg(a.exp16 + __half_as_ushort(d)))), 1048576.0f));
+      } else {
+        w = weight_q<MODE>(Lr[rr][i], mtile, a.exp16);
+      }
       run += w;
       cum[rr][i] = run;  // thread-local inclusive
       if constexpr (MODE == M_FP16) {
@@ -1691,7 +1720,9 @@ __global__ void __launch_bounds__(PF_TILE / (VPT * R), fused_min_blocks<MODE>(PF
   const float invf = MODE == M_FP16 ? __fdiv_rn(1.0f, (float)S) : 0.0f;
   const double inv = MODE == M_FP16 ? 0.0 : __ddiv_rn(1.0, (double)S);
   auto cdf_of = [&](wq_t cm) -> real {
-    if constexpr (MODE == M_FP16) {
+    if constexpr (MODE == M_FP16 && !PK) {  // naive: 1/S re-derived (cast + reciprocal) per particle
+      return (cm == S) ? __float2half(1.0f) : __float2half_rn(__fmul_rn((float)cm, rcp_f32_s64_naive((long long)S)));
+    } else if constexpr (MODE == M_FP16) {
       return (cm == S) ? __float2half(1.0f) : __float2half_rn(__fmul_rn((float)cm, invf));
     } else {
       const double cd = __dmul_rn((double)cm, inv);
