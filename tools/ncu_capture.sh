@@ -9,5 +9,5 @@ mkdir -p gpurun_out /tmp/ncu
 timeout 400 ncu -k "regex:$kre" --launch-skip "$skip" --launch-count 1 --set full --import-source on \
   --clock-control none -f -o /tmp/ncu/$name python bench.py --profile-only "$@" > gpurun_out/$name.log 2>&1
 python tools/ncu_summary.py /tmp/ncu/$name.ncu-rep "$name" > gpurun_out/$name.md 2>&1
-python tools/ncu_lines.py /tmp/ncu/$name.ncu-rep 60 > gpurun_out/${name}_lines.txt 2>&1
+python tools/ncu_lines.py /tmp/ncu/$name.ncu-rep ${NLINES:-60} > gpurun_out/${name}_lines.txt 2>&1
 if [ "$KEEP_REP" = 1 ]; then cp /tmp/ncu/$name.ncu-rep gpurun_out/; fi
