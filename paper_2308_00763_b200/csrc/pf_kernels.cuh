@@ -1443,6 +1443,7 @@ __global__ void __launch_bounds__(PF_TILE / (VPT * R), fused_min_blocks<MODE>(PF
             "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], 0;\n\t"
             "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(s_bar))
             : "memory");
+        PF_TRACE_DBG(a, 6);  // the window's CDFs have landed
       } else {  // unaligned track base (odd K with several tracks): plain copy
         for (int b = b_lo; b <= b_hi; ++b) {
           const real* src = src_C(b);
@@ -1558,6 +1559,7 @@ __global__ void __launch_bounds__(PF_TILE / (VPT * R), fused_min_blocks<MODE>(PF
           resample(std::true_type{});
         else
           resample(std::false_type{});
+        if (rr == 0) PF_TRACE_DBG(a, 7);  // thread 0's resampling search done
       }
       if (DBG && a.dbg_anc != nullptr) {
 #pragma unroll

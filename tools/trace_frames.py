@@ -18,6 +18,10 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
 
+def _q(v):
+    return f"{v.mean():.2f}/{np.percentile(v, 90):.2f}/{v.max():.2f}"
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--config", default="c2")
@@ -80,6 +84,14 @@ def main():
     d = np.diff(fu[:, :6], axis=1) / 1e3
     print("  mean per-CTA phase (us): " + ", ".join(f"{n} {v:.2f}" for n, v in zip(names, d.mean(axis=0))) +
           f"  | lifetime {(fu[:, 5] - fu[:, 0]).mean() / 1e3:.2f}")
+    # inside the particle phase (trace slots 6 / 7: window CDFs landed, thread 0's search done)
+    fu = buf[1:, :nt].reshape(-1, 8).astype(np.float64)
+    ok = (fu[:, :8] > 0).all(axis=1)
+    if ok.any():
+        g = fu[ok]
+        print(f"  particle phase split (us, mean / p90 / max): "
+              f"copy wait {_q((g[:, 6] - g[:, 3]) / 1e3)}, search {_q((g[:, 7] - g[:, 6]) / 1e3)}, "
+              f"gather..max {_q((g[:, 4] - g[:, 7]) / 1e3)}")
     t0s = np.array([r["t0"] for r in rows])
     print(f"  period (fused entry to entry): median {np.median(np.diff(t0s))/1e3:.2f} us")
     rel0 = np.array([r["t0"] + r["release"][0] * 1e3 for r in rows])
