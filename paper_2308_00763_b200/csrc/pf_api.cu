@@ -684,7 +684,9 @@ static int create_impl(pf_handle** out, const pf_config* cfg, int n_shards, int 
   const size_t NT = (size_t)h->nl * h->n_tracks;
   for (int i = 0; i < 2; ++i) {
     CK(cudack(cudaMalloc(&h->X[i], KT * h->vs), "X"));
-    CK(cudack(cudaMalloc(&h->C[i], KT * h->rs + 16), "C"));  // slack: 16-byte rounded bulk copies
+    // slack: 16-byte rounded bulk copies, and the search's 4-entry probe (up
+    // to three entries read past a track's last local CDF value)
+    CK(cudack(cudaMalloc(&h->C[i], KT * h->rs + 32), "C"));
   }
   CK(cudack(cudaMalloc(&h->rec_m, NT * 8), "rec"));
   CK(cudack(cudaMalloc(&h->rec_S, NT * 8), "rec"));
