@@ -287,6 +287,7 @@ struct pf_handle {
   ulonglong2* tt = nullptr;
   bool pdl = true;
   unsigned short* exp16 = nullptr;
+  int* exp16q = nullptr;  // rint(exp16 * 2^20): the fused FP16 kernel's weights
   void* zig = nullptr;
   int2* d_offs = nullptr;
   short* d_plan = nullptr;
@@ -517,7 +518,7 @@ int pf_destroy(pf_handle* h) {
   if (!h) return PF_OK;
   cudaSetDevice(h->device);
   void* ptrs[] = {h->X[0], h->X[1], h->C[0], h->C[1], h->rec_m, h->rec_S, h->rec_X, h->rec_Y, h->tab_s, h->tab_O,
-                  h->tab_invM, h->win, h->u, h->x0, h->tj, h->tt, h->tsync, h->tagg, h->troots, h->exp16, h->zig, h->d_offs, h->d_plan, h->d_leaves, h->d_runs, h->d_frames,
+                  h->tab_invM, h->win, h->u, h->x0, h->tj, h->tt, h->tsync, h->tagg, h->troots, h->exp16, h->exp16q, h->zig, h->d_offs, h->d_plan, h->d_leaves, h->d_runs, h->d_frames,
                   h->d_maps, h->d_traj, h->d_degen, h->dbg_anc, h->dbg_L, h->d_trace};
   for (void* p : ptrs)
     if (p) cudaFree(p);
@@ -733,6 +734,15 @@ static int create_impl(pf_handle** out, const pf_config* cfg, int n_shards, int 
   build_exp16(ex.data());
   CK(cudack(cudaMalloc(&h->exp16, 65536 * 2), "exp16"));
   CK(cudack(cudaMemcpy(h->exp16, ex.data(), 65536 * 2, cudaMemcpyHostToDevice), "exp16"));
+  {  // the same weights as weight_q<M_FP16>: rint(f32(w) * 2^20), round half to even
+    std::vector<int> exq(65536);
+    for (int i = 0; i < 65536; ++i) {
+      const double v = std::nearbyint(f16_to_f64(ex[i]) * 1048576.0);
+      exq[i] = std::isfinite(v) && v < 2147483647.0 ? (int)v : INT_MAX;
+    }
+    CK(cudack(cudaMalloc(&h->exp16q, 65536 * 4), "exp16q"));
+    CK(cudack(cudaMemcpy(h->exp16q, exq.data(), 65536 * 4, cudaMemcpyHostToDevice), "exp16q"));
+  }
   // ziggurat fast-path tables, packed for 16-byte smem staging: 256 x (ki >> 20)
   // then 256 x wi; binary16 modes: 256 x {ki >> 29, f32(wi * 2^29)} (the
   // binary32 fast path on the word's high 32 bits, oracle/rng.py)
@@ -1051,6 +1061,7 @@ static int launch_frame(pf_handle* h, const void* map_slot, long long map_video_
   a.rec_X = h->rec_X;
   a.rec_Y = h->rec_Y;
   a.exp16 = h->exp16;
+  a.exp16q = h->exp16q;
   a.drift_x = h->params.drift_x;
   a.drift_y = h->params.drift_y;
   a.std_x = h->params.std_x;

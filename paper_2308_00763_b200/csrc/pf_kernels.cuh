@@ -662,6 +662,7 @@ struct FusedArgs {
   long long* rec_X;  // fp16: int64 moments; wide: double bits
   long long* rec_Y;
   const unsigned short* exp16;
+  const int* exp16q;  // FP16 fixed-point weights: rint(exp16[d] * 2^20) per binary16 pattern d
   double drift_x, drift_y, std_x, std_y;
   long long* dbg_anc;  // optional
   void* dbg_L;         // optional
@@ -1666,6 +1667,8 @@ __global__ void __launch_bounds__(PF_TILE / (VPT * R), fused_min_blocks<MODE>(PF
       if constexpr (MODE == M_FP16 && !PK) {  // naive: per-op f32 round trips (same values)
         const __half d = hsub_s(Lr[rr][i], mtile);
         w = __float2int_rn(__fmul_rn(__half2float(__ushort_as_half(__ldg(a.exp16 + __half_as_ushort(d)))), 1048576.0f));
+      } else if constexpr (MODE == M_FP16) {  // one 32-bit table read: the weight's fixed-point value directly
+        w = __ldg(a.exp16q + __half_as_ushort(__hsub_rn(Lr[rr][i], mtile)));
       } else {
         w = weight_q<MODE>(Lr[rr][i], mtile, a.exp16);
       }
