@@ -618,7 +618,7 @@ def main():
             lat[label] = {"us_per_frame": 1e6 * (time.perf_counter() - t0) / n_lat, "frames": n_lat}
         g.close()
         step_lat = dict(lat, api="Filter.step(frame) -> (x, y): frame in, likelihood map, fused frame kernel, "
-                                 "tile table, estimate D2H, host sync -- wall clock per call",
+                                 "tile table (estimate written to host-mapped memory), host sync -- wall clock per call",
                         particles=K, precision=prec)
 
     cpu = None

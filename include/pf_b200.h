@@ -103,6 +103,10 @@ int pf_run_async(pf_handle* h, const uint8_t* frames, int32_t n_frames, int32_t 
                  void* stream);
 int pf_step_async(pf_handle* h, const uint8_t* frame, int32_t frame_on_device, double* est_out, void* stream);
 int pf_sync(pf_handle* h);
+/* Order the handle's next work after the work already queued on `stream` (a
+ * cudaStream_t of the handle's device), without a host synchronisation: e.g.
+ * before a synchronous pf_step on a device frame produced on `stream`. */
+int pf_stream_wait(pf_handle* h, void* stream);
 
 int pf_degenerate_frame(const pf_handle* h);
 

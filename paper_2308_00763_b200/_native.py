@@ -65,6 +65,7 @@ SIGNATURES = [
     ("pf_run_async", C.c_int, [_VP, _VP, C.c_int32, C.c_int32, _VP, _VP]),
     ("pf_step_async", C.c_int, [_VP, _VP, C.c_int32, _VP, _VP]),
     ("pf_sync", C.c_int, [_VP]),
+    ("pf_stream_wait", C.c_int, [_VP, _VP]),
     ("pf_degenerate_frame", C.c_int, [_VP]),
     ("pf_likelihood_maps", C.c_int, [_VP, _VP, C.c_int32, _VP]),
     ("pf_set_profiling", C.c_int, [_VP, C.c_int32]),

@@ -379,6 +379,14 @@ struct pf_handle {
   size_t h_traj_cap = 0;
   double* traj_user = nullptr;
   size_t traj_bytes = 0;
+  // one-frame synchronous steps: the tile table writes the estimate and the
+  // degeneracy flag straight into host-mapped memory (no copy back)
+  double* h_est_map = nullptr;
+  int* h_deg_map = nullptr;
+  double* d_est_map = nullptr;
+  int* d_deg_map = nullptr;
+  bool zc_step = false;     // the frame being launched is such a step
+  bool zc_pending = false;  // the enqueued run's result is in the mapped buffers
   double* noise_all = nullptr;  // [F][K][2]
   size_t noise_cap = 0;
   double* u_all = nullptr;  // [F]
@@ -535,6 +543,8 @@ int pf_destroy(pf_handle* h) {
   h->phx.release();
   if (h->h_stage) cudaFreeHost(h->h_stage);
   if (h->h_traj) cudaFreeHost(h->h_traj);
+  if (h->h_est_map) cudaFreeHost(h->h_est_map);
+  if (h->h_deg_map) cudaFreeHost(h->h_deg_map);
   if (h->noise_all) cudaFree(h->noise_all);
   if (h->u_all) cudaFree(h->u_all);
   if (h->xev) cudaEventDestroy(h->xev);
@@ -1137,6 +1147,8 @@ static int launch_frame(pf_handle* h, const void* map_slot, long long map_video_
   t.roots = h->troots;
   t.win = h->win;
   t.u_in = h->philox ? h->u_all + traj_index : nullptr;
+  t.est_host = h->zc_step ? h->d_est_map : nullptr;
+  t.deg_host = h->zc_step ? h->d_deg_map : nullptr;
   t.trace = (h->tracing && h->d_trace) ? h->d_trace + (size_t)traj_index * tr_frame + (size_t)h->n_tiles * 8 : nullptr;
   PF_CUDA(launch_pdl(h, tk, dim3(h->n_chunks, h->n_tracks), dim3(h->tpb_table), 0, t), h->err);
   PF_CUDA(cudaGetLastError(), h->err);
@@ -1310,6 +1322,20 @@ static int run_enqueue(pf_handle* h, const uint8_t* frames, int32_t F, int32_t o
     if ((rc = grow((void**)&h->d_frames, &h->frames_cap, fbytes, h->err))) return rc;
     dframes = h->d_frames;
   }
+  // a synchronous one-frame step into host memory: zero-copy result
+  h->zc_step = F == 1 && sync_call && !h->split_table && h->n_shards == 1 && std::getenv("PF_NO_ZC_STEP") == nullptr;
+  if (h->zc_step) {
+    cudaPointerAttributes at{};
+    const bool host_dst = cudaPointerGetAttributes(&at, traj_out) != cudaSuccess || at.type != cudaMemoryTypeDevice;
+    cudaGetLastError();
+    h->zc_step = host_dst;
+  }
+  if (h->zc_step && !h->h_est_map) {
+    PF_CUDA(cudaHostAlloc(&h->h_est_map, (size_t)h->n_tracks * 2 * 8, cudaHostAllocMapped), h->err);
+    PF_CUDA(cudaHostAlloc(&h->h_deg_map, (size_t)h->n_tracks * sizeof(int), cudaHostAllocMapped), h->err);
+    PF_CUDA(cudaHostGetDevicePointer(&h->d_est_map, h->h_est_map, 0), h->err);
+    PF_CUDA(cudaHostGetDevicePointer(&h->d_deg_map, h->h_deg_map, 0), h->err);
+  }
   PF_CUDA(cudaEventRecord(h->ev[0], h->stream), h->err);
   // per-frame steps: one graph launch (stage timings collapse to "frames")
   const bool step_graph = F == 1 && h->use_graphs && !h->profiling && !h->tracing && !h->dbg_anc &&
@@ -1424,6 +1450,17 @@ static int run_enqueue(pf_handle* h, const uint8_t* frames, int32_t F, int32_t o
   // pageable destination lands in pinned memory and is copied out after the sync
   const size_t tbytes = (size_t)h->n_tracks * F * 2 * 8;
   h->traj_user = nullptr;
+  h->zc_pending = false;
+  if (h->zc_step) {  // the estimate is already on its way into host-mapped memory
+    h->zc_step = false;
+    h->zc_pending = true;
+    h->traj_user = traj_out;
+    h->traj_bytes = tbytes;
+    PF_CUDA(cudaEventRecord(h->ev[4], h->stream), h->err);
+    h->pending = true;
+    h->pending_F = F;
+    return PF_OK;
+  }
   if (sync_call && is_pageable(traj_out)) {
     if (h->h_traj_cap < tbytes) {
       if (h->h_traj) cudaFreeHost(h->h_traj);
@@ -1456,7 +1493,10 @@ static int run_complete(pf_handle* h) {
   PF_CUDA(cudaStreamSynchronize(h->stream), h->err);
   h->pending = false;
   const int F = h->pending_F;
-  if (h->traj_user) {
+  if (h->zc_pending) {
+    std::memcpy(h->traj_user, h->h_est_map, h->traj_bytes);
+    h->traj_user = nullptr;
+  } else if (h->traj_user) {
     std::memcpy(h->traj_user, h->h_traj, h->traj_bytes);
     h->traj_user = nullptr;
   }
@@ -1487,6 +1527,17 @@ static int run_complete(pf_handle* h) {
   }
   cudaEventElapsedTime(&ms, h->ev[3], h->ev[4]);
   h->timings[5] = ms;
+  if (h->zc_pending) {
+    h->zc_pending = false;
+    int m = INT_MAX;
+    for (int i = 0; i < h->n_tracks; ++i) m = std::min(m, h->h_deg_map[i]);
+    if (m != INT_MAX) {
+      h->degenerate_frame = m;
+      h->err = "weight sum degenerated (frame " + std::to_string(m) + ")";
+      return PF_EDEGENERATE;
+    }
+    return PF_OK;
+  }
   return finish_degenerate(h);
 }
 
@@ -1503,6 +1554,19 @@ int pf_run_async(pf_handle* h, const uint8_t* frames, int32_t F, int32_t on_devi
 
 int pf_step_async(pf_handle* h, const uint8_t* frame, int32_t on_device, double* est_out, void* stream) {
   return run_enqueue(h, frame, 1, on_device, est_out, (cudaStream_t)stream);
+}
+
+int pf_stream_wait(pf_handle* h, void* stream) {
+  if (!h) return PF_EINVAL;
+  if (!stream) return PF_OK;
+  PF_CUDA(cudaSetDevice(h->device), h->err);
+  if (!h->xin) {
+    PF_CUDA(cudaEventCreateWithFlags(&h->xin, cudaEventDisableTiming), h->err);
+    PF_CUDA(cudaEventCreateWithFlags(&h->xout, cudaEventDisableTiming), h->err);
+  }
+  PF_CUDA(cudaEventRecord(h->xin, (cudaStream_t)stream), h->err);
+  PF_CUDA(cudaStreamWaitEvent(h->stream, h->xin, 0), h->err);
+  return PF_OK;
 }
 
 int pf_sync(pf_handle* h) {

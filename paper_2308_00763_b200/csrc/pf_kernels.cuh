@@ -31,6 +31,8 @@
 #endif
 #define PF_XQ_BITS 10
 
+#include <climits>
+
 namespace pfk {
 
 enum { M_FP64 = 0, M_FP32 = 1, M_FP16 = 2 };
@@ -574,6 +576,9 @@ __global__ void __launch_bounds__(kMapHalfThreads) pf_map_half_img(MapArgs a) {
   __syncthreads();
 
   const int npr = (a.Wm + 1) / 2, npairs = (my1 - my0) * npr;
+  // pair slots in use by this CTA (a narrow band -- one-frame steps -- fills
+  // only the first; the others are skipped, not computed on clamped indices)
+  const int kmax = min(kMapHalfPairs, (npairs + kMapHalfThreads - 1) / kMapHalfThreads);
   int base[kMapHalfPairs];
   __half2 acc[kMapHalfPairs];
 #pragma unroll
@@ -587,6 +592,7 @@ __global__ void __launch_bounds__(kMapHalfThreads) pf_map_half_img(MapArgs a) {
     const int tw = tapw[j];
 #pragma unroll
     for (int k = 0; k < kMapHalfPairs; ++k) {
+      if (k >= kmax) break;
       const unsigned v = wA[base[k] + tw];
       const __half2 tv = *reinterpret_cast<const __half2*>(&v);
       if constexpr (PK)
@@ -1841,6 +1847,8 @@ struct TableArgs {
   double* u_out;
   unsigned long long ua, uc;  // f^(t(2K+1)+2K): uniform word = ua * x0[track] + uc
   double* traj;       // [track][F][2]
+  double* est_host;   // optional: [track][2] host-mapped (one-frame steps: no copy back)
+  int* deg_host;      // optional: [track] host-mapped degeneracy flag of this frame (INT_MAX = none)
   int traj_stride;    // frames per track in traj
   int traj_index;     // frame slot
   int* degenerate;    // per track: first degenerate frame (or INT_MAX)
@@ -2168,7 +2176,13 @@ __global__ void __launch_bounds__(1024) pf_tile_table(TableArgs a) {
     tr[0] = ex;
     tr[1] = ey;
     PF_TRACE_DBG(a, 3);
-    if (!(vd > 0.0) || !isfinite(vd) || !isfinite(ex) || !isfinite(ey)) atomicMin(a.degenerate + track, a.t);
+    const bool degen = !(vd > 0.0) || !isfinite(vd) || !isfinite(ex) || !isfinite(ey);
+    if (degen) atomicMin(a.degenerate + track, a.t);
+    if (a.est_host != nullptr) {  // zero-copy result of a one-frame step (host-mapped, posted writes)
+      a.est_host[2 * track] = ex;
+      a.est_host[2 * track + 1] = ey;
+      a.deg_host[track] = degen ? a.t : INT_MAX;
+    }
     // every CTA of the track has passed the exchanges: reset them for the
     // next frame's table (which starts only after the next fused kernel
     // completes, and that ends with griddepcontrol.wait on this grid)

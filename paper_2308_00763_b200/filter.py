@@ -498,13 +498,14 @@ class Filter:
         L = N.lib()
         if on_dev:
             # device frames may still be in flight on torch's current stream:
-            # the library stream is ordered after it (stream-ordered call)
+            # the library stream is ordered after it (no host synchronisation),
+            # then the synchronous call (one-frame steps: zero-copy result)
             import torch
 
             stream = torch.cuda.current_stream(self.device).cuda_stream
-            rc = L.pf_run_async(self._h, p, F, 1, N.ptr(traj), C.c_void_p(stream))
+            rc = L.pf_stream_wait(self._h, C.c_void_p(stream))
             if rc == N.PF_OK:
-                rc = L.pf_sync(self._h)
+                rc = L.pf_run(self._h, p, F, 1, N.ptr(traj))
         else:
             rc = L.pf_run(self._h, p, F, 0, N.ptr(traj))
         del keep
