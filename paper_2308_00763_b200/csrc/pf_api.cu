@@ -314,6 +314,8 @@ struct pf_handle {
   cudaStream_t cstream = nullptr;          // host-frame uploads, chunked ahead of the maps
   cudaEvent_t cev[kUploadChunks] = {};     // per-chunk upload done
   float timings[6] = {0};
+  bool timings_stale = false;  // timings[] not yet read from the last run's events
+  int timings_F = 0;
   int64_t launches = 0;
   int degenerate_frame = -1;
   size_t map_smem = 0, fused_smem = 0, fused_smem_base = 0;
@@ -1486,24 +1488,12 @@ static int run_enqueue(pf_handle* h, const uint8_t* frames, int32_t F, int32_t o
   return PF_OK;
 }
 
-// wait for the enqueued run; timings and the degeneracy check
-static int run_complete(pf_handle* h) {
-  if (!h->pending) return PF_OK;
-  PF_CUDA(cudaSetDevice(h->device), h->err);
-  PF_CUDA(cudaStreamSynchronize(h->stream), h->err);
-  h->pending = false;
-  const int F = h->pending_F;
-  if (h->zc_pending) {
-    std::memcpy(h->traj_user, h->h_est_map, h->traj_bytes);
-    h->traj_user = nullptr;
-  } else if (h->traj_user) {
-    std::memcpy(h->traj_user, h->h_traj, h->traj_bytes);
-    h->traj_user = nullptr;
-  }
-  if (h->philox) {
-    const int rc = h->phx.check(h->err);
-    if (rc) return rc;
-  }
+// stage timings of the last completed run from its events (on demand: the
+// elapsed-time queries cost the per-frame step a few microseconds)
+static void compute_timings(pf_handle* h) {
+  if (!h->timings_stale || h->pending) return;
+  h->timings_stale = false;
+  const int F = h->timings_F;
   float ms;
   cudaEventElapsedTime(&ms, h->ev[0], h->ev[4]);
   h->timings[0] = ms;
@@ -1527,6 +1517,28 @@ static int run_complete(pf_handle* h) {
   }
   cudaEventElapsedTime(&ms, h->ev[3], h->ev[4]);
   h->timings[5] = ms;
+}
+
+// wait for the enqueued run; timings and the degeneracy check
+static int run_complete(pf_handle* h) {
+  if (!h->pending) return PF_OK;
+  PF_CUDA(cudaSetDevice(h->device), h->err);
+  PF_CUDA(cudaStreamSynchronize(h->stream), h->err);
+  h->pending = false;
+  const int F = h->pending_F;
+  if (h->zc_pending) {
+    std::memcpy(h->traj_user, h->h_est_map, h->traj_bytes);
+    h->traj_user = nullptr;
+  } else if (h->traj_user) {
+    std::memcpy(h->traj_user, h->h_traj, h->traj_bytes);
+    h->traj_user = nullptr;
+  }
+  if (h->philox) {
+    const int rc = h->phx.check(h->err);
+    if (rc) return rc;
+  }
+  h->timings_stale = true;  // event times read on demand (pf_last_timings)
+  h->timings_F = F;
   if (h->zc_pending) {
     h->zc_pending = false;
     int m = INT_MAX;
@@ -1620,6 +1632,7 @@ int pf_get_trace(pf_handle* h, uint64_t* out, int64_t n) {
 
 int pf_last_timings(const pf_handle* h, float* ms6) {
   if (!h || !ms6) return PF_EINVAL;
+  compute_timings(const_cast<pf_handle*>(h));
   for (int i = 0; i < 6; ++i) ms6[i] = h->timings[i];
   return PF_OK;
 }
