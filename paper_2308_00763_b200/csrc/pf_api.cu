@@ -1096,8 +1096,14 @@ static int launch_frame(pf_handle* h, const void* map_slot, long long map_video_
   // a non-identity frame acquires the previous table's release counter instead
   // of waiting on its predecessor grid, so it may overlap only a table kernel:
   // after the maps (or draw) kernels it is launched stream-ordered
+  // a one-frame step: launched programmatically behind its map kernel (the
+  // draws overlap the map; the map reads wait on the grid dependency --
+  // identity frames wait anyway); behind the Philox draw kernels, whose noise
+  // the draw phase reads, and in multi-frame runs it stays stream-ordered
+  const bool pdl_maps = h->serialize_next && !h->philox && traj_stride == 1 && !ordered;
+  a.wait_prev = pdl_maps && !a.ident ? 1 : 0;
   PF_CUDA(launch_pdl(h, (const void*)fused_kernel(h), dim3(h->nl, h->n_tracks), dim3(h->tpb), h->fused_smem, a,
-                     !ordered && !h->serialize_next),
+                     !ordered && (!h->serialize_next || pdl_maps)),
           h->err);
   h->serialize_next = false;
   PF_CUDA(cudaGetLastError(), h->err);

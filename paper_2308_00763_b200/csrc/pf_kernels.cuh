@@ -99,6 +99,11 @@ __device__ __forceinline__ float rcp_f32_s64_naive(long long S) {
 // TMA bulk copy helpers (cp.async.bulk + mbarrier)
 // ------------------------------------------------------------------------
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+// Programmatic dependent launch: let the next kernel in the stream start
+// early, and wait for the previous kernel's results only where they are
+// consumed (no-ops when launched without the PDL attribute).
+__device__ __forceinline__ void pdl_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 
 __device__ __forceinline__ void bulk_load_rows(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
   uint32_t b = smem_u32(bar);
@@ -178,6 +183,7 @@ __device__ __forceinline__ real term_wide(int v, real bg, real fg) {
 
 template <typename real>
 __global__ void pf_map_wide(MapArgs a) {
+  pdl_launch_dependents();  // a one-frame step's fused kernel may start its draws (it waits for the map)
   extern __shared__ __align__(16) unsigned char smem[];
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem);
   real* term = reinterpret_cast<real*>(smem + 16);
@@ -304,6 +310,7 @@ __device__ __forceinline__ void leaf_pair(const real* b0, const real* b1, const 
 
 template <typename real>
 __global__ void __launch_bounds__(1024) pf_map_wide_img(MapArgs a) {
+  pdl_launch_dependents();  // a one-frame step's fused kernel may start its draws (it waits for the map)
   extern __shared__ __align__(16) unsigned char smem[];
   const MapWideGeom g = map_wide_geom(a.W, a.r, a.n_off, (int)sizeof(real), a.band);
   real* term = reinterpret_cast<real*>(smem);
@@ -367,6 +374,7 @@ __host__ __device__ inline MapRunsGeom map_runs_geom(int W, int r, int n_runs, i
 
 template <typename real>
 __global__ void __launch_bounds__(1024) pf_map_wide_runs(MapArgs a) {
+  pdl_launch_dependents();  // a one-frame step's fused kernel may start its draws (it waits for the map)
   extern __shared__ __align__(16) unsigned char smem[];
   const MapRunsGeom g = map_runs_geom(a.W, a.r, a.n_runs, a.band);
   int* term = reinterpret_cast<int*>(smem);
@@ -435,6 +443,7 @@ __global__ void __launch_bounds__(1024) pf_map_wide_runs(MapArgs a) {
 // entries per thread in one half2.
 #ifndef PF_FUSED_ONLY  // launched from pf_api.cu only
 __global__ void pf_map_half(MapArgs a) {
+  pdl_launch_dependents();  // a one-frame step's fused kernel may start its draws (it waits for the map)
   extern __shared__ __align__(16) unsigned char smem[];
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem);
   __half* term = reinterpret_cast<__half*>(smem + 16);
@@ -520,6 +529,7 @@ __host__ __device__ inline MapHalfGeom map_half_geom(int W, int H, int r, int n_
 
 template <bool PK>  // PK: one HADD2 per entry pair and tap; else two scalar HADDs (same values)
 __global__ void __launch_bounds__(kMapHalfThreads) pf_map_half_img(MapArgs a) {
+  pdl_launch_dependents();  // a one-frame step's fused kernel may start its draws (it waits for the map)
   extern __shared__ __align__(16) unsigned char smem[];
   const MapHalfGeom g = map_half_geom(a.W, a.H, a.r, a.n_off, a.band);
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem);
@@ -679,6 +689,7 @@ struct FusedArgs {
   unsigned long long* tmax;   // per track (stride 4): [0] order key of the running max of the tile maxima,
                               //   [1] table-ready counter (+1 per table chunk and frame)
   unsigned long long ready_target;  // frame t > 0 proceeds once tmax[1] >= this (n_chunks * t)
+  int wait_prev;                    // launched behind the map kernel (PDL): grid-dependency wait before the map reads
   unsigned long long* trace;  // optional: [tile][8] %globaltimer stamps (track 0)
   const double2* noise;       // NZ variants: this frame's draws (n, d) per particle (the reference's
                               //   own stream, generated by pf_philox.cuh), one track
@@ -708,12 +719,6 @@ __device__ __forceinline__ double okey_inv(unsigned long long k) {
   const unsigned long long b = (k & 0x8000000000000000ULL) ? (k & 0x7fffffffffffffffULL) : ~k;
   return __longlong_as_double((long long)b);
 }
-
-// Programmatic dependent launch: let the next kernel in the stream start
-// early, and wait for the previous kernel's results only where they are
-// consumed (no-ops when launched without the PDL attribute).
-__device__ __forceinline__ void pdl_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
-__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 
 template <typename T>
 __device__ __forceinline__ T shfl_up(T v, int d) {
@@ -1368,6 +1373,9 @@ __global__ void __launch_bounds__(PF_TILE / (VPT * R), fused_min_blocks<MODE>(PF
           // frame's critical path)
           asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(rc) : "memory");
         }
+        // launched programmatically behind the map kernel (one-frame step):
+        // the frame's map is complete only after the grid dependency wait
+        if (a.wait_prev) pdl_wait();
       }
       __syncwarp();
     } else {
