@@ -332,6 +332,7 @@ struct pf_handle {
   int g_cur = -1, g_F = -1;
   const void* g_maps = nullptr;
   const void* g_traj = nullptr;
+  const void* g_est = nullptr;  // host-mapped trajectory the run graph's tables write (or null)
   // sharding (pf_shard_*): this handle holds global tiles [tile0, tile0 + nl)
   long long Kl = 0;  // particles per track held here (== K unless sharded)
   int nl = 0;        // tiles per track held here (== n_tiles unless sharded)
@@ -383,11 +384,12 @@ struct pf_handle {
   size_t traj_bytes = 0;
   // one-frame synchronous steps: the tile table writes the estimate and the
   // degeneracy flag straight into host-mapped memory (no copy back)
-  double* h_est_map = nullptr;
-  int* h_deg_map = nullptr;
+  double* h_est_map = nullptr;  // [track][frame][2] trajectory of the run
+  size_t est_map_cap = 0;       // bytes
+  int* h_deg_map = nullptr;     // [track] first degenerate frame of the run (INT_MAX = none)
   double* d_est_map = nullptr;
   int* d_deg_map = nullptr;
-  bool zc_step = false;     // the frame being launched is such a step
+  bool zc_step = false;     // the run being launched writes its results to the mapped buffers
   bool zc_pending = false;  // the enqueued run's result is in the mapped buffers
   double* noise_all = nullptr;  // [F][K][2]
   size_t noise_cap = 0;
@@ -1155,7 +1157,7 @@ static int launch_frame(pf_handle* h, const void* map_slot, long long map_video_
   t.roots = h->troots;
   t.win = h->win;
   t.u_in = h->philox ? h->u_all + traj_index : nullptr;
-  t.est_host = h->zc_step ? h->d_est_map : nullptr;
+  t.est_host = h->zc_step ? h->d_est_map : nullptr;  // indexed like traj
   t.deg_host = h->zc_step ? h->d_deg_map : nullptr;
   t.trace = (h->tracing && h->d_trace) ? h->d_trace + (size_t)traj_index * tr_frame + (size_t)h->n_tiles * 8 : nullptr;
   PF_CUDA(launch_pdl(h, tk, dim3(h->n_chunks, h->n_tracks), dim3(h->tpb_table), 0, t), h->err);
@@ -1290,6 +1292,7 @@ static int step_graph_launch(pf_handle* h, const uint8_t* dframes, int on_device
   return PF_OK;
 }
 
+static int run_complete(pf_handle* h);
 static int run_enqueue(pf_handle* h, const uint8_t* frames, int32_t F, int32_t on_device, double* traj_out,
                        cudaStream_t ext, bool sync_call = false) {
   if (!h || !frames || F < 1 || !traj_out) return PF_EINVAL;
@@ -1331,18 +1334,34 @@ static int run_enqueue(pf_handle* h, const uint8_t* frames, int32_t F, int32_t o
     dframes = h->d_frames;
   }
   // a synchronous one-frame step into host memory: zero-copy result
-  h->zc_step = F == 1 && sync_call && !h->split_table && h->n_shards == 1 && std::getenv("PF_NO_ZC_STEP") == nullptr;
+  // (any synchronous run into host memory: the tile tables write the
+  // trajectory and the degeneracy flags into host-mapped memory)
+  h->zc_step = sync_call && !h->split_table && h->n_shards == 1 && !h->profiling &&
+               std::getenv("PF_NO_ZC_STEP") == nullptr;
   if (h->zc_step) {
     cudaPointerAttributes at{};
     const bool host_dst = cudaPointerGetAttributes(&at, traj_out) != cudaSuccess || at.type != cudaMemoryTypeDevice;
     cudaGetLastError();
     h->zc_step = host_dst;
   }
-  if (h->zc_step && !h->h_est_map) {
-    PF_CUDA(cudaHostAlloc(&h->h_est_map, (size_t)h->n_tracks * 2 * 8, cudaHostAllocMapped), h->err);
-    PF_CUDA(cudaHostAlloc(&h->h_deg_map, (size_t)h->n_tracks * sizeof(int), cudaHostAllocMapped), h->err);
-    PF_CUDA(cudaHostGetDevicePointer(&h->d_est_map, h->h_est_map, 0), h->err);
-    PF_CUDA(cudaHostGetDevicePointer(&h->d_deg_map, h->h_deg_map, 0), h->err);
+  if (h->zc_step) {
+    const size_t need = (size_t)h->n_tracks * F * 2 * 8;
+    if (h->est_map_cap < need) {
+      if (h->pending) run_complete(h);
+      PF_CUDA(cudaStreamSynchronize(h->stream), h->err);
+      if (h->h_est_map) cudaFreeHost(h->h_est_map);
+      h->h_est_map = nullptr;
+      h->est_map_cap = 0;
+      PF_CUDA(cudaHostAlloc(&h->h_est_map, need, cudaHostAllocMapped), h->err);
+      h->est_map_cap = need;
+      PF_CUDA(cudaHostGetDevicePointer(&h->d_est_map, h->h_est_map, 0), h->err);
+    }
+    if (!h->h_deg_map) {
+      PF_CUDA(cudaHostAlloc(&h->h_deg_map, (size_t)h->n_tracks * sizeof(int), cudaHostAllocMapped), h->err);
+      PF_CUDA(cudaHostGetDevicePointer(&h->d_deg_map, h->h_deg_map, 0), h->err);
+    }
+    if (h->pending) run_complete(h);  // the flags below are the previous run's until it completes
+    for (int i = 0; i < h->n_tracks; ++i) h->h_deg_map[i] = INT_MAX;
   }
   PF_CUDA(cudaEventRecord(h->ev[0], h->stream), h->err);
   // per-frame steps: one graph launch (stage timings collapse to "frames")
@@ -1413,7 +1432,7 @@ static int run_enqueue(pf_handle* h, const uint8_t* frames, int32_t F, int32_t o
   const bool graph_ok = h->use_graphs && !h->profiling && F >= 4;
   if (graph_ok && h->gexec && h->g_start == h->frame_counter && h->g_cur == h->cur && h->g_F == F &&
       h->g_maps == h->d_maps && h->g_traj == h->d_traj && h->g_ident == h->ident_next &&
-      h->g_noise == (const void*)h->noise_all) {
+      h->g_noise == (const void*)h->noise_all && h->g_est == (h->zc_step ? (const void*)h->d_est_map : nullptr)) {
     PF_CUDA(cudaGraphLaunch(h->gexec, h->stream), h->err);
     h->ident_next = false;
     h->frame_counter += F;
@@ -1445,6 +1464,7 @@ static int run_enqueue(pf_handle* h, const uint8_t* frames, int32_t F, int32_t o
     h->g_F = F;
     h->g_maps = h->d_maps;
     h->g_traj = h->d_traj;
+    h->g_est = h->zc_step ? (const void*)h->d_est_map : nullptr;
     PF_CUDA(cudaGraphLaunch(h->gexec, h->stream), h->err);
   } else {
     for (int f = 0; f < F; ++f) {

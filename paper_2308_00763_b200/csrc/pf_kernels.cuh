@@ -1855,8 +1855,8 @@ struct TableArgs {
   double* u_out;
   unsigned long long ua, uc;  // f^(t(2K+1)+2K): uniform word = ua * x0[track] + uc
   double* traj;       // [track][F][2]
-  double* est_host;   // optional: [track][2] host-mapped (one-frame steps: no copy back)
-  int* deg_host;      // optional: [track] host-mapped degeneracy flag of this frame (INT_MAX = none)
+  double* est_host;   // optional: host-mapped copy of traj (synchronous runs: no copy back)
+  int* deg_host;      // optional: [track] host-mapped first degenerate frame of the run (INT_MAX = none)
   int traj_stride;    // frames per track in traj
   int traj_index;     // frame slot
   int* degenerate;    // per track: first degenerate frame (or INT_MAX)
@@ -2186,10 +2186,11 @@ __global__ void __launch_bounds__(1024) pf_tile_table(TableArgs a) {
     PF_TRACE_DBG(a, 3);
     const bool degen = !(vd > 0.0) || !isfinite(vd) || !isfinite(ex) || !isfinite(ey);
     if (degen) atomicMin(a.degenerate + track, a.t);
-    if (a.est_host != nullptr) {  // zero-copy result of a one-frame step (host-mapped, posted writes)
-      a.est_host[2 * track] = ex;
-      a.est_host[2 * track + 1] = ey;
-      a.deg_host[track] = degen ? a.t : INT_MAX;
+    if (a.est_host != nullptr) {  // zero-copy result of a synchronous run (host-mapped, posted writes)
+      double* eh = a.est_host + ((size_t)track * a.traj_stride + a.traj_index) * 2;
+      eh[0] = ex;
+      eh[1] = ey;
+      if (degen && a.deg_host[track] > a.t) a.deg_host[track] = a.t;  // the host set INT_MAX before the run
     }
     // every CTA of the track has passed the exchanges: reset them for the
     // next frame's table (which starts only after the next fused kernel
