@@ -598,20 +598,26 @@ __global__ void __launch_bounds__(kMapHalfThreads) pf_map_half_img(MapArgs a) {
     base[k] = row * (g.P / 2) + x2;
     acc[k] = __float2half2_rn(0.0f);
   }
-  for (int j = 0; j < a.n_off; ++j) {
-    const int tw = tapw[j];
+  auto taps = [&](auto full_tag) {
+    constexpr bool FULL = decltype(full_tag)::value;
+    for (int j = 0; j < a.n_off; ++j) {
+      const int tw = tapw[j];
 #pragma unroll
-    for (int k = 0; k < kMapHalfPairs; ++k) {
-      if (k >= kmax) break;
-      const unsigned v = wA[base[k] + tw];
-      const __half2 tv = *reinterpret_cast<const __half2*>(&v);
-      if constexpr (PK)
-        acc[k] = __hadd2_rn(acc[k], tv);
-      else
-        acc[k] = __halves2half2(hadd_s(__low2half(acc[k]), __low2half(tv)), hadd_s(__high2half(acc[k]), __high2half(tv)));
-
+      for (int k = 0; k < kMapHalfPairs; ++k) {
+        if (!FULL && k >= kmax) break;
+        const unsigned v = wA[base[k] + tw];
+        const __half2 tv = *reinterpret_cast<const __half2*>(&v);
+        if constexpr (PK)
+          acc[k] = __hadd2_rn(acc[k], tv);
+        else
+          acc[k] = __halves2half2(hadd_s(__low2half(acc[k]), __low2half(tv)), hadd_s(__high2half(acc[k]), __high2half(tv)));
+      }
     }
-  }
+  };
+  if (kmax == kMapHalfPairs)  // every pair slot in use (multi-frame maps): no per-slot test
+    taps(std::true_type{});
+  else
+    taps(std::false_type{});
   __half* out = reinterpret_cast<__half*>(a.maps) + (size_t)vf * a.Hm * a.Wm;
 #pragma unroll
   for (int k = 0; k < kMapHalfPairs; ++k) {
