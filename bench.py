@@ -425,12 +425,21 @@ def main():
 
     import torch
 
+    # PF_BENCH_SHARE_GPU=1 (test hook): more ranks than GPUs -- ranks share
+    # devices round-robin and synchronise over gloo (NCCL needs one GPU per
+    # rank); exercises the N-rank path on a one-GPU box.  Not a measurement.
+    share = os.environ.get("PF_BENCH_SHARE_GPU") == "1"
+    if share:
+        local = local % torch.cuda.device_count()
     torch.cuda.set_device(local)
     dist = None
     if world > 1:
         import torch.distributed as dist
 
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if share:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     import paper_2308_00763_b200 as pf
 
     from paper_2308_00763_b200.sharding import max_over_ranks, shard_tracks
