@@ -371,6 +371,16 @@ def systematic_ancestors(cdf: np.ndarray, u: float, device: int = 0) -> np.ndarr
 # ---------------------------------------------------------------------------
 
 
+def _current_stream(device: int) -> int:
+    """torch's current CUDA stream on `device` (raw cudaStream_t)."""
+    import torch
+
+    raw = getattr(torch._C, "_cuda_getCurrentRawStream", None)  # one call, no Stream object
+    if raw is not None:
+        return int(raw(device))
+    return torch.cuda.current_stream(device).cuda_stream
+
+
 class Filter:
     """Fused one-launch-per-frame filter on one device.
 
@@ -500,10 +510,7 @@ class Filter:
             # device frames may still be in flight on torch's current stream:
             # the library stream is ordered after it (no host synchronisation),
             # then the synchronous call (one-frame steps: zero-copy result)
-            import torch
-
-            stream = torch.cuda.current_stream(self.device).cuda_stream
-            rc = L.pf_stream_wait(self._h, C.c_void_p(stream))
+            rc = L.pf_stream_wait(self._h, C.c_void_p(_current_stream(self.device)))
             if rc == N.PF_OK:
                 rc = L.pf_run(self._h, p, F, 1, N.ptr(traj))
         else:
