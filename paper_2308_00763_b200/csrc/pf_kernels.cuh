@@ -1142,9 +1142,12 @@ __device__ __forceinline__ double tree_vpt(const double* v) {
 #ifndef PF_MINB_FP16_256
 #define PF_MINB_FP16_256 7  // A/B knob (make EXTRA=-DPF_MINB_FP16_256=6)
 #endif
+#ifndef PF_MINB_FP16_128
+#define PF_MINB_FP16_128 0  // A/B knob (0: the compiler's choice)
+#endif
 template <int MODE>
 constexpr int fused_min_blocks(int tpb) {
-  return tpb == 128 ? (MODE == M_FP32 ? 7 : MODE == M_FP64 ? 6 : 0)
+  return tpb == 128 ? (MODE == M_FP32 ? 7 : MODE == M_FP64 ? 6 : PF_MINB_FP16_128)
          : tpb != 256 ? 0 : MODE == M_FP16 ? PF_MINB_FP16_256 : MODE == M_FP32 ? 6 : 4;  // 0: no constraint
 }
 
@@ -1573,7 +1576,15 @@ __global__ void __launch_bounds__(PF_TILE / (VPT * R), fused_min_blocks<MODE>(PF
               const double q = gM == 0.0 ? 0.0 : __dmul_rn(__dsub_rn(p, gO), gM);
               kq = KT::up(fmin(fmax(q, 0.0), 1.0));
             }
-            int j = jprev >= 0 ? advance_key<MODE, (MODE == M_FP16 && VPT < 8)>(cb, jprev, tb, kq) : lb_first<MODE, VPT>(cb, tb, kq);
+            // the unrolled first search is emitted once (particle 0); a later
+            // particle that starts a new source tile (rare) takes the loop
+            int j;
+            if (i == 0)
+              j = lb_first<MODE, VPT>(cb, tb, kq);
+            else if (jprev >= 0)
+              j = advance_key<MODE, (MODE == M_FP16 && VPT < 8)>(cb, jprev, tb, kq);
+            else
+              j = lb_branchless<MODE>(cb, tb, kq);
             j = min(j, tb - 1);
             jprev = j;
             anc[i] = tl + j;
