@@ -1347,7 +1347,10 @@ static int run_enqueue(pf_handle* h, const uint8_t* frames, int32_t F, int32_t o
   if (h->zc_step) {
     const size_t need = (size_t)h->n_tracks * F * 2 * 8;
     if (h->est_map_cap < need) {
-      if (h->pending) run_complete(h);
+      if (h->pending) {
+        const int prc = run_complete(h);
+        if (prc) return prc;
+      }
       PF_CUDA(cudaStreamSynchronize(h->stream), h->err);
       if (h->h_est_map) cudaFreeHost(h->h_est_map);
       h->h_est_map = nullptr;
@@ -1360,7 +1363,10 @@ static int run_enqueue(pf_handle* h, const uint8_t* frames, int32_t F, int32_t o
       PF_CUDA(cudaHostAlloc(&h->h_deg_map, (size_t)h->n_tracks * sizeof(int), cudaHostAllocMapped), h->err);
       PF_CUDA(cudaHostGetDevicePointer(&h->d_deg_map, h->h_deg_map, 0), h->err);
     }
-    if (h->pending) run_complete(h);  // the flags below are the previous run's until it completes
+    if (h->pending) {  // the flags below are the previous run's until it completes (its error is reported here)
+      const int prc = run_complete(h);
+      if (prc) return prc;
+    }
     for (int i = 0; i < h->n_tracks; ++i) h->h_deg_map[i] = INT_MAX;
   }
   PF_CUDA(cudaEventRecord(h->ev[0], h->stream), h->err);
