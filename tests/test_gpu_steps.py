@@ -79,3 +79,31 @@ def test_steps_on_reference_stream_and_tracks(pf, video):
     steps = np.stack([g.step(vids[:, t]) for t in range(frames.shape[0])], axis=1)
     assert np.array_equal(steps, ref3)
     g.close()
+
+
+@pytest.mark.parametrize("mode", ["fp64", "fp32"])
+def test_fused_degeneracy_reported(pf, video, mode):
+    """A degenerate frame (here: NaN positions injected with set_state, so the
+    weighted estimate is not finite) raises DegeneracyError with that frame's
+    index -- through a whole run and through per-frame steps (the tile table
+    reports it through host-mapped memory for synchronous calls), and the
+    handle recovers after reset().  (Binary16 modes keep exact integer
+    moments of rint(x * 2^10): a NaN position converts to 0 there, and every
+    tile's maximum weight is 2^20 > 0, so the stabilised filter cannot
+    degenerate.)"""
+    frames, _ = video
+    K = 4096
+    f = pf.Filter(K, mode, 128, 128, 42)
+    nan = np.full(K, np.nan)
+    f.set_state(nan, nan, 3)
+    with pytest.raises(pf.DegeneracyError) as info:
+        f.run(frames[3:8])
+    assert info.value.frame == 3
+    f.set_state(nan, nan, 5)
+    with pytest.raises(pf.DegeneracyError) as info:
+        f.step(frames[5])
+    assert info.value.frame == 5
+    f.reset()
+    ref = pf.Filter(K, mode, 128, 128, 42).run(frames)
+    assert np.array_equal(f.run(frames), ref)
+    f.close()
